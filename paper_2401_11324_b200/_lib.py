@@ -1,0 +1,131 @@
+"""ctypes binding of libbang.so (the C-ABI declared in include/bang.h).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+visible, every entry point raises :class:`BangError` loudly.  The library is
+built in-tree by ``__graft_entry__.build()`` (nvcc, sm_100a).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import BangError, ParameterError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbang.so")
+
+BANG_OK = 0
+BANG_E_PARAM = -1
+BANG_E_CUDA = -2
+BANG_E_OOM = -3
+BANG_E_CAPACITY = -4
+BANG_E_STATE = -5
+
+VEC_F32, VEC_U8, VEC_I8 = 0, 1, 2
+GRAPH_HBM, GRAPH_HOST_MAPPED = 0, 1
+
+RERANK = 1
+DEBUG_CHECKS = 2
+EXACT_DISTANCE = 4
+TABLE_GLOBAL = 8
+TABLE_SMEM = 16
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+
+
+class SearchStats(ctypes.Structure):
+    _fields_ = [
+        ("queries", ctypes.c_int64), ("iterations", ctypes.c_int64),
+        ("probes", ctypes.c_int64), ("fresh", ctypes.c_int64),
+        ("rerank_cands", ctypes.c_int64), ("retries", ctypes.c_int64),
+        ("slots", ctypes.c_int32), ("warps_per_cta", ctypes.c_int32),
+        ("ctas", ctypes.c_int32), ("adc_variant", ctypes.c_int32),
+        ("kernel_ms", ctypes.c_float), ("table_ms", ctypes.c_float),
+        ("algorithmic_bytes", ctypes.c_int64), ("adc_bytes", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_SIGS = {
+    "bang_last_error": (ctypes.c_char_p, []),
+    "bang_version": (ctypes.c_char_p, []),
+    "bang_device_count": (_I32, []),
+    "bang_index_create": (_I32, [_I32, _P, _I64, _I32, _P, _P, _I32, _P, _P, _I32, _I32, _P,
+                                 _I32, _I32, ctypes.POINTER(_P)]),
+    "bang_index_destroy": (None, [_P]),
+    "bang_index_info": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "bang_index_device_ptrs": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "bang_search": (_I32, [_P, _P, _I64, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P, _P,
+                           _P, _I64]),
+    "bang_last_visit_logs": (_I32, [_P, _P, _I64]),
+    "bang_last_search_stats": (_I32, [_P, ctypes.POINTER(SearchStats)]),
+    "bang_index_set_log_capacity": (_I32, [_P, _I64]),
+    "bang_search_device": (_I32, [_P, _P, _I64, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P]),
+    "bang_sync_status": (_I32, [_P]),
+    "bang_pq_table_device": (_I32, [_P, _P, _I32, _I32, _P, _I64, _P, _P]),
+    "bang_bloom_filter_device": (_I32, [_P, _I64, _I64, _P, _P, _P, _P]),
+    "bang_adc_device": (_I32, [_P, _I32, _P, _P, _P, _I64, _P, _P, _P]),
+    "bang_sort_rows_device": (_I32, [_P, _I64, _I32, _P]),
+    "bang_merge_rows_device": (_I32, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
+    "bang_worklist_update_device": (_I32, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
+    "bang_rerank_device": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
+    "bang_exact_sq_dists_device": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Load libbang.so once; raise BangError if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BangError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                            "(there is no CPU fallback for the search path)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().bang_last_error().decode("utf-8", "replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a bang_status onto the reference's exception classes."""
+    if status == BANG_OK:
+        return
+    msg = last_error() or what
+    if status == BANG_E_PARAM:
+        raise ParameterError(msg)
+    raise BangError(f"{what}: {msg} (status {status})" if what else msg)
+
+
+def device_count() -> int:
+    return int(lib().bang_device_count())
+
+
+def ptr(a):
+    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def stream_ptr(stream):
+    if stream is None:
+        return None
+    return ctypes.c_void_p(int(getattr(stream, "cuda_stream", stream)))

@@ -1,0 +1,417 @@
+// bang_device.cuh -- device building blocks of the B200 BANG search path.
+//
+// Each function restates one piece of the reference's arithmetic (paths
+// under /root/reference/pkg/src/bang/) so that every result is bit-exact:
+//   f32 distance-table entries without FMA ....... pq.py:284-296
+//   sequential f32 ADC sums over s = 0..m-1 ....... engine.py:99-105
+//   FNV-1a-64 Bloom slots + test-and-set .......... bloom.py:26-42, 101-163
+//   (f32 bits << 32 | id) keys and their order .... kernels.py:1-41
+//   f64-accumulated exact distances -> f32 ....... engine.py:48-51
+// They are shared by the fused persistent search kernel and by the
+// stand-alone per-kernel entry points in bang_kernels.cuh.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bang {
+
+constexpr uint64_t kSentinel = 0xFFFFFFFFFFFFFFFFull;
+constexpr uint64_t kFnvOffset = 0xCBF29CE484222325ull;
+constexpr uint64_t kFnvPrime = 0x100000001B3ull;
+// h2 starts from FNV-1a of the prefix byte 0x5A (bloom.py:31-32)
+constexpr uint64_t kFnvOffsetH2 = (kFnvOffset ^ 0x5Aull) * kFnvPrime;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+enum VecDtype { kVecF32 = 0, kVecU8 = 1, kVecI8 = 2 };
+enum AdcVariant { kAdcSmemCodebook = 0, kAdcGlobalTable = 1, kAdcExact = 2 };
+
+// kernels.py:25-29 -- non-negative f32 bit patterns are monotone, so the
+// u64 order is the (dist, id) lexicographic order.
+__host__ __device__ __forceinline__ uint64_t pack_key(float d, uint32_t id) {
+#ifdef __CUDA_ARCH__
+    return (static_cast<uint64_t>(__float_as_uint(d)) << 32) | id;
+#else
+    uint32_t b;
+    __builtin_memcpy(&b, &d, 4);
+    return (static_cast<uint64_t>(b) << 32) | id;
+#endif
+}
+__device__ __forceinline__ float key_dist(uint64_t k) { return __uint_as_float((uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_id(uint64_t k) { return (uint32_t)(k & 0xFFFFFFFFull); }
+
+// bloom.py:26-34 -- FNV-1a-64 over the id's four little-endian bytes.
+__host__ __device__ __forceinline__ uint64_t fnv1a(uint32_t id, uint64_t h) {
+#pragma unroll
+    for (int s = 0; s < 32; s += 8) h = (h ^ ((id >> s) & 0xFFu)) * kFnvPrime;
+    return h;
+}
+
+// h mod z for a runtime z < 2^32 without the 64-bit division subroutine:
+// magic = floor((2^64-1)/z) makes umulhi(h, magic) either floor(h/z) or one
+// less (the truncation error is < 1), so one conditional subtract is exact.
+struct BloomGeom {
+    uint64_t z;
+    uint64_t magic;
+};
+__device__ __forceinline__ uint32_t mod_z(uint64_t h, const BloomGeom &g) {
+    uint64_t q = __umul64hi(h, g.magic);
+    uint64_t r = h - q * g.z;
+    if (r >= g.z) r -= g.z;
+    return (uint32_t)r;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(kFull, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------- Bloom
+// One warp test-and-sets one row's probes (up to NPL*32 ids, probe i lives
+// in lane i%32, register i/32) against one filter of u32 words.
+// Semantics = sequential test-and-set in probe order (bloom.py:124-163):
+//  1. every probe tests the PRE-state (two L2 loads, issued together);
+//  2. fresh probes set their bits with fetch-or atomics; a bit that a
+//     different fresh probe of this row set first shows up in the returned
+//     old word while it was clear in the pre-state -- exactly the in-row
+//     slot sharing that bloom.py:134-158 detects;
+//  3. on any such collision (rare: ~0.3% of rows at z = 399,887) the
+//     touched words are restored to the pre-state and the row is replayed
+//     in order by lane 0 (bloom.py:110-122) -- bit-exact, unlike the
+//     paper's tolerated race.
+// The filter is read through L2 (ld.global.cg) because it is written by
+// atomics performed at L2 during the same kernel.
+template <int NPL>
+__device__ __forceinline__ void bloom_test_and_set(uint32_t *__restrict__ bits,
+                                                   const BloomGeom &g,
+                                                   const uint32_t (&ids)[NPL], int cnt,
+                                                   bool (&fresh)[NPL]) {
+    const int lane = (int)lane_id();
+    uint32_t p1[NPL], p2[NPL], w1[NPL], w2[NPL];
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        fresh[k] = false;
+        p1[k] = p2[k] = w1[k] = w2[k] = 0;
+        if (lane + 32 * k < cnt) {
+            p1[k] = mod_z(fnv1a(ids[k], kFnvOffset), g);
+            p2[k] = mod_z(fnv1a(ids[k], kFnvOffsetH2), g);
+            w1[k] = __ldcg(bits + (p1[k] >> 5));
+            w2[k] = __ldcg(bits + (p2[k] >> 5));
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NPL; ++k)
+        if (lane + 32 * k < cnt)
+            fresh[k] = !(((w1[k] >> (p1[k] & 31)) & 1u) && ((w2[k] >> (p2[k] & 31)) & 1u));
+    __syncwarp();  // every pre-state load has landed before any atomic
+    bool coll = false;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        if (fresh[k]) {
+            const uint32_t b1 = 1u << (p1[k] & 31);
+            const uint32_t o1 = atomicOr(bits + (p1[k] >> 5), b1);
+            coll |= (o1 & b1) && !(w1[k] & b1);
+            if (p2[k] != p1[k]) {
+                const uint32_t b2 = 1u << (p2[k] & 31);
+                const uint32_t o2 = atomicOr(bits + (p2[k] >> 5), b2);
+                coll |= (o2 & b2) && !(w2[k] & b2);
+            }
+        }
+    }
+    if (__any_sync(kFull, coll)) {
+        // restore the pre-state of every word a fresh probe touched
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            if (fresh[k]) {
+                __stcg(bits + (p1[k] >> 5), w1[k]);
+                __stcg(bits + (p2[k] >> 5), w2[k]);
+            }
+        }
+        __threadfence_block();
+        __syncwarp();
+        uint32_t mask[NPL];
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            mask[k] = 0;
+            const int n = min(32, cnt - 32 * k);
+            for (int j = 0; j < n; ++j) {
+                const uint32_t id = __shfl_sync(kFull, ids[k], j);
+                if (lane == 0) {
+                    const uint32_t q1 = mod_z(fnv1a(id, kFnvOffset), g);
+                    const uint32_t q2 = mod_z(fnv1a(id, kFnvOffsetH2), g);
+                    const uint32_t b1 = 1u << (q1 & 31), b2 = 1u << (q2 & 31);
+                    const bool hit = (__ldcg(bits + (q1 >> 5)) & b1) && (__ldcg(bits + (q2 >> 5)) & b2);
+                    if (!hit) {
+                        atomicOr(bits + (q1 >> 5), b1);
+                        atomicOr(bits + (q2 >> 5), b2);
+                        mask[k] |= 1u << j;
+                    }
+                }
+            }
+            mask[k] = __shfl_sync(kFull, mask[k], 0);
+            fresh[k] = (mask[k] >> lane) & 1u;
+        }
+    }
+    __syncwarp();  // this row's sets are ordered before the next row's tests
+}
+
+// ------------------------------------------------------- distance table
+// pq.py:290-294: diff = q - c; diff *= diff; acc = diff[0]; acc += diff[j].
+// Intrinsics keep every op separately rounded (no FFMA contraction).
+__device__ __forceinline__ float table_entry(const float *__restrict__ q,
+                                             const float *__restrict__ c, int size) {
+    float d = __fsub_rn(q[0], c[0]);
+    float acc = __fmul_rn(d, d);
+    for (int j = 1; j < size; ++j) {
+        d = __fsub_rn(q[j], c[j]);
+        acc = __fadd_rn(acc, __fmul_rn(d, d));
+    }
+    return acc;
+}
+__device__ __forceinline__ float table_entry2(float2 q, float2 c) {
+    float d0 = __fsub_rn(q.x, c.x), d1 = __fsub_rn(q.y, c.y);
+    return __fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1));
+}
+__device__ __forceinline__ float table_entry4(float4 q, float4 c) {
+    float d0 = __fsub_rn(q.x, c.x), d1 = __fsub_rn(q.y, c.y);
+    float d2 = __fsub_rn(q.z, c.z), d3 = __fsub_rn(q.w, c.w);
+    float acc = __fadd_rn(__fmul_rn(d0, d0), __fmul_rn(d1, d1));
+    acc = __fadd_rn(acc, __fmul_rn(d2, d2));
+    return __fadd_rn(acc, __fmul_rn(d3, d3));
+}
+
+// ------------------------------------------------------------------ ADC
+// engine.py:99-105: acc = 0f; acc += T[s][code[s]] for s = 0..m-1 (f32).
+// Variant A (smem codebook): T[s][c] is recomputed from the CTA-resident
+// codebook and the warp's query in exactly pq.py's op order, so it equals
+// the table entry bit-for-bit (verified by the parity tests).
+// SUB > 0: uniform subspace width; MV > 0: m = 16*MV, code rows read as MV
+// 16-byte vectors (north_star's vectorised code gather).
+template <int SUB, int MV>
+__device__ __forceinline__ float adc_codebook(const float *__restrict__ s_cb,
+                                              const float *__restrict__ s_q,
+                                              const int *__restrict__ s_off,
+                                              const int *__restrict__ s_sz, int m,
+                                              const uint8_t *__restrict__ code_row) {
+    float acc = 0.0f;
+    if constexpr (SUB > 0 && MV > 0) {
+        uint4 cv[MV];
+#pragma unroll
+        for (int v = 0; v < MV; ++v) cv[v] = __ldg(reinterpret_cast<const uint4 *>(code_row) + v);
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            const uint32_t w[4] = {cv[v].x, cv[v].y, cv[v].z, cv[v].w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const int s = v * 16 + b;
+                const uint32_t c = (w[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
+                float e;
+                if constexpr (SUB == 4) {
+                    e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                                     *reinterpret_cast<const float4 *>(s_cb + (s * 256 + c) * 4));
+                } else if constexpr (SUB == 2) {
+                    e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                                     *reinterpret_cast<const float2 *>(s_cb + (s * 256 + c) * 2));
+                } else {
+                    e = table_entry(s_q + s * SUB, s_cb + (s * 256 + c) * SUB, SUB);
+                }
+                acc = __fadd_rn(acc, e);
+            }
+        }
+    } else {
+        for (int s = 0; s < m; ++s) {
+            const int c = __ldg(code_row + s);
+            const int off = s_off[s], sz = s_sz[s];
+            acc = __fadd_rn(acc, table_entry(s_q + off, s_cb + off * 256 + c * sz, sz));
+        }
+    }
+    return acc;
+}
+
+// Variant B (HBM table from kernel 1): the reference's literal data flow.
+template <int MV>
+__device__ __forceinline__ float adc_table(const float *__restrict__ trow, int m,
+                                           const uint8_t *__restrict__ code_row) {
+    float acc = 0.0f;
+    if constexpr (MV > 0) {
+        uint4 cv[MV];
+#pragma unroll
+        for (int v = 0; v < MV; ++v) cv[v] = __ldg(reinterpret_cast<const uint4 *>(code_row) + v);
+#pragma unroll
+        for (int v = 0; v < MV; ++v) {
+            const uint32_t w[4] = {cv[v].x, cv[v].y, cv[v].z, cv[v].w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const int s = v * 16 + b;
+                const uint32_t c = (w[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
+                acc = __fadd_rn(acc, __ldg(trow + s * 256 + c));
+            }
+        }
+    } else {
+        for (int s = 0; s < m; ++s) acc = __fadd_rn(acc, __ldg(trow + s * 256 + __ldg(code_row + s)));
+    }
+    return acc;
+}
+
+// ------------------------------------------------------ exact distances
+// Plain loads: the vectors may live in pinned, mapped host memory.
+// engine.py:48-51: widen to f32 (validation.py:38-43), f64 difference,
+// f64 sum of squares in dimension order, round to f32.  (numpy's einsum
+// sums in a SIMD order; the rounded f32 agrees -- SURVEY.md 8(c).)
+__device__ __forceinline__ float exact_sq_dist(const void *__restrict__ vectors, int dtype,
+                                               int dim, int64_t row,
+                                               const float *__restrict__ q) {
+    double acc = 0.0;
+    if (dtype == kVecF32) {
+        const float *x = reinterpret_cast<const float *>(vectors) + row * (int64_t)dim;
+        if ((dim & 3) == 0) {
+            for (int j = 0; j < dim; j += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(x + j);
+                const float xs[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const double d = __dsub_rn((double)xs[u], (double)q[j + u]);
+                    acc = __dadd_rn(acc, __dmul_rn(d, d));
+                }
+            }
+        } else {
+            for (int j = 0; j < dim; ++j) {
+                const double d = __dsub_rn((double)x[j], (double)q[j]);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+        }
+    } else {
+        const uint8_t *x = reinterpret_cast<const uint8_t *>(vectors) + row * (int64_t)dim;
+        const bool sgn = dtype == kVecI8;
+        if ((dim & 3) == 0) {
+            for (int j = 0; j < dim; j += 4) {
+                const uint32_t v = *reinterpret_cast<const uint32_t *>(x + j);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t b = (v >> (8 * u)) & 0xFFu;
+                    const float xf = sgn ? (float)(int8_t)b : (float)b;
+                    const double d = __dsub_rn((double)xf, (double)q[j + u]);
+                    acc = __dadd_rn(acc, __dmul_rn(d, d));
+                }
+            }
+        } else {
+            for (int j = 0; j < dim; ++j) {
+                const uint32_t b = x[j];
+                const float xf = sgn ? (float)(int8_t)b : (float)b;
+                const double d = __dsub_rn((double)xf, (double)q[j]);
+                acc = __dadd_rn(acc, __dmul_rn(d, d));
+            }
+        }
+    }
+    return __double2float_rn(acc);
+}
+
+// ------------------------------------------------------- sorted arrays
+// number of entries of sorted a[0, n) strictly below x
+__device__ __forceinline__ int lower_bound_u64(const uint64_t *a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+// number of entries of sorted a[0, n) at or below x
+__device__ __forceinline__ int upper_bound_u64(const uint64_t *a, int n, uint64_t x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// first index i in [from, cnt) with vis[i] == 0 (cnt if none); warp-uniform
+__device__ __forceinline__ int first_unvisited(const uint8_t *s_vis, int from, int cnt) {
+    const int lane = (int)lane_id();
+    for (int b = from; b < cnt; b += 32) {
+        const int i = b + lane;
+        const unsigned m = __ballot_sync(kFull, i < cnt && !s_vis[i]);
+        if (m) return b + __ffs(m) - 1;
+    }
+    return cnt;
+}
+
+// ------------------------------------------------ worklist sort + merge
+// kernels.py:44-109 / engine.py:210-215 for one warp-owned worklist in smem.
+//   s_wl[0, cnt) sorted keys, s_vis flags; new keys key[c] (lane + 32c < F,
+//   unique, unsorted, SENTINEL elsewhere); s_sk scratch (>= F entries).
+// Keys in wl u new are unique (the Bloom filter has no false negatives), so
+// any correct merge is bit-identical to the reference's rank merge with its
+// a-first tie rule.  Sort = rank counting over warp shuffles; merge = each
+// element's final rank = own rank + rank in the other list (the paper's
+// Merge_LSet), written in place chunk by chunk from the
+// top so no unread entry is overwritten; entries ranked >= t are dropped.
+// Returns the new count min(t, cnt + F).
+template <int NPL>
+__device__ __forceinline__ int worklist_merge(uint64_t *s_wl, uint8_t *s_vis, int cnt, int t,
+                                              const uint64_t (&key)[NPL], int F,
+                                              uint64_t *s_sk) {
+    const int lane = (int)lane_id();
+    int r1[NPL];
+#pragma unroll
+    for (int c = 0; c < NPL; ++c) r1[c] = 0;
+#pragma unroll
+    for (int cs = 0; cs < NPL; ++cs) {
+        if (32 * cs < F) {
+            const int n = min(32, F - 32 * cs);
+            for (int i = 0; i < n; ++i) {
+                const uint64_t ki = __shfl_sync(kFull, key[cs], i);
+#pragma unroll
+                for (int c = 0; c < NPL; ++c) r1[c] += ki < key[c];
+            }
+        }
+    }
+    int newpos[NPL];
+#pragma unroll
+    for (int c = 0; c < NPL; ++c) {
+        newpos[c] = t;  // dropped
+        if (lane + 32 * c < F) {
+            s_sk[r1[c]] = key[c];
+            newpos[c] = r1[c] + lower_bound_u64(s_wl, cnt, key[c]);
+        }
+    }
+    __syncwarp();
+    const int nch = (cnt + 31) >> 5;
+    for (int ch = nch - 1; ch >= 0; --ch) {
+        const int i = ch * 32 + lane;
+        uint64_t v = 0;
+        uint8_t vv = 0;
+        int dst = t;
+        if (i < cnt) {
+            v = s_wl[i];
+            vv = s_vis[i];
+            dst = i + lower_bound_u64(s_sk, F, v);
+        }
+        __syncwarp();
+        if (dst < t) {
+            s_wl[dst] = v;
+            s_vis[dst] = vv;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int c = 0; c < NPL; ++c) {
+        if (newpos[c] < t) {
+            s_wl[newpos[c]] = key[c];
+            s_vis[newpos[c]] = 0;
+        }
+    }
+    __syncwarp();
+    return min(t, cnt + F);
+}
+
+}  // namespace bang

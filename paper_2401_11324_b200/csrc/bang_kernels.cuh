@@ -1,0 +1,561 @@
+// bang_kernels.cuh -- sm_100a kernels of the BANG search path.
+//
+//   search_kernel          the fused persistent batched search (kernels 2-5
+//                          + eager prefetch in one kernel, one warp per query)
+//   pq_table_kernel        kernel 1, build_pq_dist_table   (pq.py:284-319)
+//   bloom_bank_kernel      kernel 2, filter_and_set        (bloom.py:124-163)
+//   adc_kernel             kernel 3, _pq_point_dists+pack  (engine.py:99-105)
+//   sort_rows_kernel       kernel 4a, merge_sort_rows      (kernels.py:94-109)
+//   merge_rows_kernel      kernel 4b, merge_rows           (kernels.py:68-87)
+//   worklist_update_kernel kernel 4, engine step           (engine.py:201-217)
+//   rerank_kernel          kernel 5, re-rank               (engine.py:244-262)
+//   exact_dists_kernel     exact_sq_dists                  (engine.py:48-51)
+#pragma once
+
+#include "bang_device.cuh"
+
+namespace bang {
+
+// counters[] slots of the fused kernel
+enum Counter {
+    kCtrNextQuery = 0,
+    kCtrIterations = 1,
+    kCtrProbes = 2,
+    kCtrFresh = 3,
+    kCtrRerank = 4,
+    kCtrOverflow = 5,
+    kCtrDebugFail = 6,
+    kCtrT0 = 7,
+    kCtrCount = 8,
+};
+
+struct SearchParams {
+    // index (HBM, or host-mapped for the graph/vectors)
+    const uint8_t *codes;
+    const float *centroids;  // concat (256, sub_s) f32 over s
+    const int32_t *sub_off;  // m (dimension offsets)
+    const int32_t *sub_size; // m
+    const float *table;      // (nq_map, m, 256) for kAdcGlobalTable, indexed by query id
+    const int32_t *adj;      // (n, R) int32, -1 padded
+    const int32_t *deg;      // (n,)
+    const void *vectors;     // (n, dim) f32/u8/i8
+    // batch
+    const float *queries;       // (nq_total, dim)
+    const int32_t *query_map;   // optional: queries to search this pass
+    int64_t nq;                 // queries this pass
+    // outputs (indexed by query id)
+    int32_t *out_ids;
+    float *out_dists;
+    int32_t *out_iters;
+    uint8_t *out_short;
+    uint64_t *out_wall_ns;
+    int32_t *visit_log;  // (nq_total, log_cap)
+    int64_t log_cap;
+    uint64_t *rr_scratch;  // (slots, log_cap) re-rank keys
+    int32_t *overflow_list;
+    // per-slot Bloom filters
+    uint32_t *bloom;
+    int64_t bloom_stride;  // u32 words per slot (multiple of 4)
+    BloomGeom geom;
+    uint32_t medoid_p1, medoid_p2;
+    unsigned long long *counters;
+    // shapes
+    int32_t m, dim, R, medoid, k, t, vec_dtype, adc_variant, rerank, debug;
+    int32_t smem_shared_bytes, per_warp_bytes;
+    int32_t off_q, off_wl, off_sk, off_fid, off_vis;  // byte offsets inside a warp region
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void record_t0_kernel(unsigned long long *counters) {
+    counters[kCtrT0] = globaltimer_ns();
+}
+
+// Score one candidate for the warp's query (ADC or exact distance).
+template <int SUB, int MV>
+__device__ __forceinline__ float score_node(const SearchParams &p, const float *s_cb,
+                                            const int *s_off, const int *s_sz,
+                                            const float *s_q, int64_t qid, uint32_t node) {
+    if (p.adc_variant == kAdcSmemCodebook)
+        return adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)node * p.m);
+    if (p.adc_variant == kAdcGlobalTable)
+        return adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)node * p.m);
+    return exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q);
+}
+
+// Top-k of unique keys keys[0, L) (global, written by this warp) into
+// out_ids/out_dists; k rounds of a warp-wide min above the last pick.
+__device__ __forceinline__ void warp_topk_write(const uint64_t *keys, int64_t L, int k,
+                                                int32_t *out_ids, float *out_dists) {
+    const int lane = (int)lane_id();
+    uint64_t last = 0;
+    for (int j = 0; j < k; ++j) {
+        uint64_t local = kSentinel;
+        if (j < L) {
+            for (int64_t i = lane; i < L; i += 32) {
+                const uint64_t v = __ldcg(reinterpret_cast<const unsigned long long *>(keys) + i);
+                if ((j == 0 || v > last) && v < local) local = v;
+            }
+        }
+        const uint64_t sel = warp_min_u64(local);
+        if (lane == 0) {
+            if (sel != kSentinel) {
+                out_ids[j] = (int32_t)key_id(sel);
+                out_dists[j] = key_dist(sel);
+            } else {
+                out_ids[j] = -1;
+                out_dists[j] = __int_as_float(0x7f800000);
+            }
+        }
+        last = sel;
+    }
+}
+
+// -------------------------------------------------------------------------
+// The fused persistent search kernel.  One warp owns one query at a time
+// (dynamic fetch from an atomic counter, so stragglers never idle an SM);
+// per-query state: worklist + visited flags + query vector in shared
+// memory, Bloom filter in HBM/L2, adjacency row of the next candidate in
+// registers.  Per iteration (engine.py:152-236):
+//   expand u -> Bloom test-and-set of u's neighbours (kernel 2) -> ADC of
+//   the fresh ones (kernel 3) -> eager winner = min(best fresh, first
+//   unvisited) and the winner's adjacency row is loaded NOW ("one hop
+//   ahead") -> sort + merge-truncate to t (kernel 4)
+//   -> converged when no unvisited entry is left.
+// At convergence the warp re-ranks its visit log with exact distances
+// (kernel 5) and writes the query's outputs.
+// -------------------------------------------------------------------------
+template <int NPL, int SUB, int MV>
+__global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = (int)lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int slot = blockIdx.x * nwarps + warp;
+
+    float *s_cb = reinterpret_cast<float *>(smem);
+    int *s_off = nullptr, *s_sz = nullptr;
+    if (p.adc_variant == kAdcSmemCodebook) {
+        const int n4 = (256 * p.dim) / 4;
+        const float4 *src = reinterpret_cast<const float4 *>(p.centroids);
+        float4 *dst = reinterpret_cast<float4 *>(s_cb);
+        for (int i = threadIdx.x; i < n4; i += blockDim.x) dst[i] = __ldg(src + i);
+        s_off = reinterpret_cast<int *>(smem + (size_t)256 * p.dim * 4);
+        s_sz = s_off + p.m;
+        if (!(SUB > 0 && MV > 0)) {
+            for (int i = threadIdx.x; i < p.m; i += blockDim.x) {
+                s_off[i] = p.sub_off[i];
+                s_sz[i] = p.sub_size[i];
+            }
+        }
+        __syncthreads();
+    }
+    unsigned char *wbase = smem + p.smem_shared_bytes + (size_t)warp * p.per_warp_bytes;
+    float *s_q = reinterpret_cast<float *>(wbase + p.off_q);
+    uint64_t *s_wl = reinterpret_cast<uint64_t *>(wbase + p.off_wl);
+    uint64_t *s_sk = reinterpret_cast<uint64_t *>(wbase + p.off_sk);
+    uint32_t *s_fid = reinterpret_cast<uint32_t *>(wbase + p.off_fid);
+    uint8_t *s_vis = wbase + p.off_vis;
+    uint32_t *bits = p.bloom + (int64_t)slot * p.bloom_stride;
+    uint64_t *rr = p.rr_scratch + (int64_t)slot * p.log_cap;
+    const int t = p.t, R = p.R;
+
+    unsigned long long st_iters = 0, st_probes = 0, st_fresh = 0, st_rr = 0;
+
+    for (;;) {
+        int64_t qi = 0;
+        if (lane == 0) qi = (int64_t)atomicAdd(p.counters + kCtrNextQuery, 1ull);
+        qi = __shfl_sync(kFull, qi, 0);
+        if (qi >= p.nq) break;
+        const int64_t qid = p.query_map ? (int64_t)p.query_map[qi] : qi;
+
+        // query vector -> smem; clear this slot's filter; set the medoid
+        // (engine.py:127-128 set_all_rows)
+        for (int j = lane; j < p.dim; j += 32) s_q[j] = __ldg(p.queries + qid * p.dim + j);
+        {
+            uint4 *b4 = reinterpret_cast<uint4 *>(bits);
+            const int64_t n4 = p.bloom_stride >> 2;
+            const uint4 z4 = make_uint4(0, 0, 0, 0);
+            for (int64_t i = lane; i < n4; i += 32) __stcg(b4 + i, z4);
+        }
+        for (int j = lane; j < t; j += 32) s_vis[j] = 0;
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) {
+            atomicOr(bits + (p.medoid_p1 >> 5), 1u << (p.medoid_p1 & 31));
+            atomicOr(bits + (p.medoid_p2 >> 5), 1u << (p.medoid_p2 & 31));
+        }
+        // worklist = [key(score(medoid), medoid)] (engine.py:118-125)
+        float d0 = 0.f;
+        if (lane == 0) d0 = score_node<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, (uint32_t)p.medoid);
+        d0 = __shfl_sync(kFull, d0, 0);
+        if (lane == 0) s_wl[0] = pack_key(d0, (uint32_t)p.medoid);
+        int cnt = 1, upos = 0;
+        uint32_t u = (uint32_t)p.medoid;
+        uint32_t ids[NPL];
+        int deg = p.deg[u];
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            const int c = lane + 32 * k;
+            ids[k] = c < R ? (uint32_t)p.adj[(int64_t)u * R + c] : 0u;
+        }
+        // log rows follow the pass order when a query map is given (retry pass)
+        int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
+        int iters = 0;
+        __syncwarp();
+
+        for (;;) {
+            // ---- expand u (engine.py:163-178)
+            if (p.debug && lane == 0 && key_id(s_wl[upos]) != u)
+                atomicAdd(p.counters + kCtrDebugFail, 1ull);
+            if (lane == 0) {
+                s_vis[upos] = 1;
+                if (iters < p.log_cap) log[iters] = (int32_t)u;
+            }
+            ++iters;
+            st_probes += deg;
+            // ---- kernel 2: Bloom test-and-set in adjacency order (engine.py:180-186)
+            bool fresh[NPL];
+            bloom_test_and_set<NPL>(bits, p.geom, ids, deg, fresh);
+            // ---- compact the fresh ids (warp-aggregated ballot + popc)
+            int F = 0;
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) {
+                const unsigned b = __ballot_sync(kFull, fresh[k]);
+                if (fresh[k]) s_fid[F + __popc(b & ((1u << lane) - 1u))] = ids[k];
+                F += __popc(b);
+            }
+            st_fresh += F;
+            __syncwarp();
+            // ---- kernel 3: ADC of the fresh neighbours (engine.py:188-199)
+            uint64_t key[NPL];
+#pragma unroll
+            for (int c = 0; c < NPL; ++c) {
+                key[c] = kSentinel;
+                const int j = lane + 32 * c;
+                if (j < F) {
+                    const uint32_t node = s_fid[j];
+                    key[c] = pack_key(score_node<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, node), node);
+                }
+            }
+            // ---- eager winner (engine.py:201-205) and one-hop-ahead prefetch
+            uint64_t best = key[0];
+#pragma unroll
+            for (int c = 1; c < NPL; ++c) best = key[c] < best ? key[c] : best;
+            best = warp_min_u64(best);
+            const int hpos = first_unvisited(s_vis, upos + 1, cnt);
+            const uint64_t head = hpos < cnt ? s_wl[hpos] : kSentinel;
+            const uint64_t winner = best < head ? best : head;
+            uint32_t nids[NPL];
+            int ndeg = 0;
+            if (winner != kSentinel) {
+                const uint32_t w = key_id(winner);
+                ndeg = p.deg[w];
+#pragma unroll
+                for (int k = 0; k < NPL; ++k) {
+                    const int c = lane + 32 * k;
+                    nids[k] = c < R ? (uint32_t)p.adj[(int64_t)w * R + c] : 0u;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < NPL; ++k) nids[k] = 0u;
+            }
+            // ---- kernel 4: sort + merge + truncate (engine.py:210-215)
+            cnt = worklist_merge<NPL>(s_wl, s_vis, cnt, t, key, F, s_sk);
+            // ---- converge (engine.py:217-236)
+            upos = first_unvisited(s_vis, 0, cnt);
+            if (upos >= cnt) break;
+            if (p.debug && lane == 0 && s_wl[upos] != winner) atomicAdd(p.counters + kCtrDebugFail, 1ull);
+            u = key_id(winner);
+            deg = ndeg;
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) ids[k] = nids[k];
+        }
+        st_iters += iters;
+
+        // ---- outputs (engine.py:244-269)
+        int32_t *oid = p.out_ids + qid * p.k;
+        float *odist = p.out_dists + qid * p.k;
+        if (lane == 0) {
+            p.out_iters[qid] = iters;
+            p.out_wall_ns[qid] = globaltimer_ns() - p.counters[kCtrT0];
+        }
+        if (p.rerank && p.adc_variant != kAdcExact) {
+            if (iters > p.log_cap) {  // visit log truncated: the host re-runs this query
+                if (lane == 0) {
+                    const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+                    p.overflow_list[at] = (int32_t)qid;
+                }
+                continue;
+            }
+            // kernel 5: exact distances of the visit log, then top-k
+            __syncwarp();
+            for (int i = lane; i < iters; i += 32) {
+                const uint32_t node = (uint32_t)__ldcg(log + i);
+                rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+            }
+            st_rr += iters;
+            __threadfence_block();
+            __syncwarp();
+            warp_topk_write(rr, iters, p.k, oid, odist);
+            if (lane == 0) p.out_short[qid] = iters < p.k;
+        } else {
+            if (p.log_cap < iters && lane == 0) {
+                const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+                p.overflow_list[at] = (int32_t)qid;
+            }
+            for (int j = lane; j < p.k; j += 32) {
+                if (j < cnt) {
+                    oid[j] = (int32_t)key_id(s_wl[j]);
+                    odist[j] = key_dist(s_wl[j]);
+                } else {
+                    oid[j] = -1;
+                    odist[j] = __int_as_float(0x7f800000);
+                }
+            }
+            if (lane == 0) p.out_short[qid] = cnt < p.k;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        atomicAdd(p.counters + kCtrIterations, st_iters);
+        atomicAdd(p.counters + kCtrProbes, st_probes);
+        atomicAdd(p.counters + kCtrFresh, st_fresh);
+        atomicAdd(p.counters + kCtrRerank, st_rr);
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 1 -- build_pq_dist_table (pq.py:284-319).  One CTA per query,
+// thread c = centroid c, subspaces in order; each subspace row (1 KB) is
+// written coalesced.  Exact f32 op order, no FMA.
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pq_table_kernel(const float *__restrict__ centroids,
+                                                       const int32_t *__restrict__ sub_off,
+                                                       const int32_t *__restrict__ sub_size,
+                                                       int m, int dim,
+                                                       const float *__restrict__ queries,
+                                                       float *__restrict__ out) {
+    extern __shared__ float s_qt[];
+    const int64_t q = blockIdx.x;
+    for (int j = threadIdx.x; j < dim; j += blockDim.x) s_qt[j] = __ldg(queries + q * dim + j);
+    __syncthreads();
+    const int c = threadIdx.x;
+    float *o = out + q * (int64_t)m * 256;
+    for (int s = 0; s < m; ++s) {
+        const int off = __ldg(sub_off + s), sz = __ldg(sub_size + s);
+        const float *cc = centroids + (int64_t)off * 256 + (int64_t)c * sz;
+        float d = __fsub_rn(s_qt[off], __ldg(cc));
+        float acc = __fmul_rn(d, d);
+        for (int j = 1; j < sz; ++j) {
+            d = __fsub_rn(s_qt[off + j], __ldg(cc + j));
+            acc = __fadd_rn(acc, __fmul_rn(d, d));
+        }
+        __stcs(o + s * 256 + c, acc);
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 2 -- BloomFilterBank.filter_and_set (bloom.py:124-163): one warp
+// per filter row, the row's probes processed 32 at a time in order.
+// -------------------------------------------------------------------------
+__global__ void bloom_bank_kernel(uint32_t *bits, int64_t count, int64_t words32, BloomGeom g,
+                                  const int64_t *__restrict__ row_off,
+                                  const uint32_t *__restrict__ ids, uint8_t *fresh) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row >= count) return;
+    const int lane = (int)lane_id();
+    uint32_t *b = bits + row * words32;
+    const int64_t lo = row_off[row], hi = row_off[row + 1];
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int cnt = (int)min((int64_t)32, hi - base);
+        uint32_t id[1] = {lane < cnt ? ids[base + lane] : 0u};
+        bool fr[1];
+        bloom_test_and_set<1>(b, g, id, cnt, fr);
+        if (lane < cnt) fresh[base + lane] = fr[0] ? 1 : 0;
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 3 -- ADC over (query row, node) pairs (engine.py:99-105) with the
+// key pack of engine.py:195-199.  One thread per pair, code row gathered as
+// 16-byte vectors when m % 16 == 0.
+// -------------------------------------------------------------------------
+template <int MV>
+__global__ void adc_kernel(const float *__restrict__ table, int m,
+                           const uint8_t *__restrict__ codes, const int64_t *__restrict__ qrows,
+                           const uint32_t *__restrict__ ids, int64_t n, float *dists,
+                           uint64_t *keys) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t node = __ldg(ids + i);
+    const float d = adc_table<MV>(table + __ldg(qrows + i) * (int64_t)m * 256, m,
+                                  codes + (int64_t)node * m);
+    if (dists) dists[i] = d;
+    if (keys) keys[i] = pack_key(d, node);
+}
+
+// -------------------------------------------------------------------------
+// Kernel 4a -- merge_sort_rows (kernels.py:94-109).  One CTA per row; each
+// element's stable rank (#less + #equal-before) is its output slot, which
+// yields exactly the ascending row for any width.
+// -------------------------------------------------------------------------
+__global__ void sort_rows_kernel(uint64_t *keys, int w) {
+    extern __shared__ uint64_t s_row[];
+    uint64_t *row = keys + (int64_t)blockIdx.x * w;
+    for (int i = threadIdx.x; i < w; i += blockDim.x) s_row[i] = row[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < w; i += blockDim.x) {
+        const uint64_t v = s_row[i];
+        int r = 0;
+        for (int j = 0; j < w; ++j) {
+            const uint64_t x = s_row[j];
+            r += (x < v) || (x == v && j < i);
+        }
+        row[r] = v;
+    }
+}
+
+// Kernel 4b -- merge_rows (kernels.py:68-87): a_i -> i + #{b < a_i};
+// b_j -> j + #{a <= b_j} (the reference's rank merge, a first on ties).
+__global__ void merge_rows_kernel(const uint64_t *__restrict__ a, const uint8_t *__restrict__ a_pay,
+                                  int wa, const uint64_t *__restrict__ b, int wb, uint64_t *out,
+                                  uint8_t *out_pay) {
+    const int64_t r = blockIdx.x;
+    const uint64_t *ar = a + r * wa, *br = b + r * wb;
+    uint64_t *o = out + r * (int64_t)(wa + wb);
+    uint8_t *op = out_pay ? out_pay + r * (int64_t)(wa + wb) : nullptr;
+    for (int i = threadIdx.x; i < wa; i += blockDim.x) {
+        const int pos = i + lower_bound_u64(br, wb, ar[i]);
+        o[pos] = ar[i];
+        if (op) op[pos] = a_pay ? a_pay[r * wa + i] : 0;
+    }
+    for (int j = threadIdx.x; j < wb; j += blockDim.x) {
+        const int pos = j + upper_bound_u64(ar, wa, br[j]);
+        o[pos] = br[j];
+        if (op) op[pos] = 0;
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 4 (engine step) -- eager pick + sort + merge + truncate + converge
+// (engine.py:201-217) per worklist row, one warp per row, through the same
+// worklist_merge the fused kernel runs.
+// -------------------------------------------------------------------------
+template <int NPL>
+__global__ void worklist_update_kernel(uint64_t *wl_keys, uint8_t *wl_vis, int64_t rows, int t,
+                                       const uint64_t *__restrict__ new_keys, int w,
+                                       uint64_t *winner, uint8_t *done) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (row >= rows) return;
+    const int per_warp = ((t * 8 + 15) & ~15) + ((NPL * 32 * 8 + 15) & ~15) + ((t + 15) & ~15);
+    unsigned char *base = smem + (size_t)warp * per_warp;
+    uint64_t *s_wl = reinterpret_cast<uint64_t *>(base);
+    uint64_t *s_sk = reinterpret_cast<uint64_t *>(base + ((t * 8 + 15) & ~15));
+    uint8_t *s_vis = base + ((t * 8 + 15) & ~15) + ((NPL * 32 * 8 + 15) & ~15);
+    uint64_t *gw = wl_keys + row * t;
+    uint8_t *gv = wl_vis + row * t;
+    int cnt = 0;
+    for (int b = 0; b < t; b += 32) {
+        const int i = b + lane;
+        bool real = false;
+        if (i < t) {
+            s_wl[i] = gw[i];
+            s_vis[i] = gv[i];
+            real = gw[i] != kSentinel;
+        }
+        cnt += __popc(__ballot_sync(kFull, real));
+    }
+    // new keys: compact the non-sentinel ones into lanes
+    uint64_t key[NPL];
+    int F = 0;
+#pragma unroll
+    for (int c = 0; c < NPL; ++c) key[c] = kSentinel;
+    for (int b = 0; b < w; b += 32) {
+        const int i = b + lane;
+        const uint64_t v = i < w ? new_keys[row * w + i] : kSentinel;
+        const unsigned m = __ballot_sync(kFull, v != kSentinel);
+        const int pos = F + __popc(m & ((1u << lane) - 1u));
+        // place v into (pos % 32, pos / 32) via smem staging
+        if (v != kSentinel) s_sk[pos] = v;
+        F += __popc(m);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NPL; ++c)
+        if (lane + 32 * c < F) key[c] = s_sk[lane + 32 * c];
+    __syncwarp();
+    uint64_t best = key[0];
+#pragma unroll
+    for (int c = 1; c < NPL; ++c) best = key[c] < best ? key[c] : best;
+    best = warp_min_u64(best);
+    const int hpos = first_unvisited(s_vis, 0, cnt);
+    const uint64_t head = hpos < cnt ? s_wl[hpos] : kSentinel;
+    const uint64_t win = best < head ? best : head;
+    cnt = worklist_merge<NPL>(s_wl, s_vis, cnt, t, key, F, s_sk);
+    const int upos = first_unvisited(s_vis, 0, cnt);
+    for (int i = lane; i < t; i += 32) {
+        gw[i] = i < cnt ? s_wl[i] : kSentinel;
+        gv[i] = i < cnt ? s_vis[i] : 0;
+    }
+    if (lane == 0) {
+        winner[row] = win;
+        done[row] = upos >= cnt ? 1 : 0;
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 5 -- re-rank (engine.py:244-262): one warp per query over its
+// candidates; keys staged in `scratch` (same CSR layout).
+// -------------------------------------------------------------------------
+__global__ void rerank_kernel(const void *vectors, int dtype, int dim,
+                              const float *__restrict__ queries, int64_t nq,
+                              const int64_t *__restrict__ off, const int32_t *__restrict__ cand,
+                              uint64_t *scratch, int k, int32_t *out_ids, float *out_dists,
+                              uint8_t *out_short) {
+    extern __shared__ float s_qr[];
+    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (q >= nq) return;
+    float *sq = s_qr + (size_t)warp * dim;
+    for (int j = lane; j < dim; j += 32) sq[j] = queries[q * dim + j];
+    __syncwarp();
+    const int64_t lo = off[q], L = off[q + 1] - lo;
+    for (int64_t i = lane; i < L; i += 32) {
+        const uint32_t node = (uint32_t)cand[lo + i];
+        scratch[lo + i] = pack_key(exact_sq_dist(vectors, dtype, dim, node, sq), node);
+    }
+    __threadfence_block();
+    __syncwarp();
+    warp_topk_write(scratch + lo, L, k, out_ids + q * k, out_dists + q * k);
+    if (lane == 0) out_short[q] = L < k;
+}
+
+// Visit-log compaction: row r of a (rows, cap) log -> CSR at out + off[dst(r)],
+// dst(r) = map ? map[r] : r.  One warp per row.
+__global__ void compact_logs_kernel(const int32_t *__restrict__ log, int64_t cap, int64_t rows,
+                                    const int32_t *__restrict__ map, const int64_t *__restrict__ off,
+                                    const uint8_t *__restrict__ skip, int32_t *out) {
+    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= rows) return;
+    const int64_t q = map ? map[r] : r;
+    if (skip && skip[q]) return;
+    const int64_t lo = off[q], len = off[q + 1] - lo;
+    for (int64_t i = lane_id(); i < len; i += 32) out[lo + i] = log[r * cap + i];
+}
+
+// exact_sq_dists (engine.py:48-51), row-paired, one thread per row.
+__global__ void exact_dists_kernel(const void *points, int dtype, int dim,
+                                   const float *__restrict__ queries, int64_t n, float *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = exact_sq_dist(points, dtype, dim, i, queries + i * dim);
+}
+
+}  // namespace bang

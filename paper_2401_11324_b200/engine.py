@@ -1,0 +1,303 @@
+"""Drop-in batched search engine: the reference's GraphSearcher API
+(engine.py:335-460) over the B200 kernels of libbang.so.
+
+``fit`` uploads the index once (codes + codebook + graph + re-rank vectors
+to HBM, or graph/vectors pinned+mapped in host memory for
+``mode="pipelined"``); ``search`` runs each ``batch_size`` chunk through the
+fused persistent search kernel (bang_search) and returns the reference's
+``SearchResult``.  Results equal the reference's bit for bit: visit logs,
+iterations, ids, distances, short flags (tests/test_gpu_parity.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib
+from .bloom import DEFAULT_ENTRIES
+from .errors import BangError, ParameterError
+from .graph import GraphIndex
+from .kernels import SENTINEL, merge_sort_rows, pack_keys, unpack_keys, _next_pow2
+from .pq import CompressedVectors, PQCodebook
+from .validation import as_engine_rows, as_float32_rows, check_matrix, check_positive
+
+try:  # the reference is a scikit-learn estimator; keep get_params/clone working
+    from sklearn.base import BaseEstimator
+except ImportError:  # pragma: no cover
+    class BaseEstimator:  # minimal stand-in with the same params protocol
+        def get_params(self, deep=True):
+            import inspect
+            names = [p for p in inspect.signature(self.__init__).parameters if p != "self"]
+            return {n: getattr(self, n) for n in names}
+
+MODES = ("pipelined", "in_memory", "exact_distance")
+_VEC_CODE = {np.dtype(np.float32): _lib.VEC_F32, np.dtype(np.uint8): _lib.VEC_U8,
+             np.dtype(np.int8): _lib.VEC_I8}
+
+
+@dataclass
+class SearchResult:
+    """Per-query outputs of a batched search (engine.py:85-96)."""
+
+    ids: np.ndarray          # (nq, k) int32, -1 padding when short
+    dists: np.ndarray        # (nq, k) float32, +inf padding
+    iterations: np.ndarray   # (nq,) int32
+    converged: np.ndarray    # (nq,) bool
+    wall_times: np.ndarray   # (nq,) float64, seconds from batch start (device clock)
+    elapsed: float           # total search seconds over all batches
+    short: np.ndarray        # (nq,) bool
+    visit_logs: list         # per query, expanded node ids in visit order (int64)
+
+
+class IndexHost:
+    """The host domain of the reference (engine.py:54-72): graph + vectors."""
+
+    def __init__(self, graph: GraphIndex, vectors: np.ndarray):
+        vectors = check_matrix(vectors, "vectors")
+        if vectors.shape[0] != graph.node_count:
+            raise ParameterError("vector count does not match the graph")
+        self.graph = graph
+        self.vectors = vectors
+
+    def fetch(self, node_ids):
+        ids = np.asarray(node_ids, dtype=np.int64)
+        return (self.graph.adjacency[ids], self.graph.degrees[ids],
+                as_float32_rows(self.vectors[ids]))
+
+
+class DeviceIndex:
+    """Owner of one ``bang_index`` handle (one GPU)."""
+
+    def __init__(self, graph: GraphIndex, vectors: np.ndarray, codebook: PQCodebook | None,
+                 codes: CompressedVectors | None, placement: int, device: int | None = None):
+        L = _lib.lib()
+        self.device = _dev.device_index() if device is None else int(device)
+        vec = as_engine_rows(vectors)
+        self.dim = vec.shape[1]
+        self.n = graph.node_count
+        if codebook is not None:
+            cb = codebook.concatenated()
+            sizes = np.ascontiguousarray(codebook.subspace_sizes, dtype=np.int32)
+            cds = np.ascontiguousarray(codes.codes, dtype=np.uint8)
+            m = codebook.m
+        else:
+            cb = sizes = cds = None
+            m = 0
+        handle = ctypes.c_void_p()
+        adj = np.ascontiguousarray(graph.adjacency, dtype=np.int32)
+        deg = np.ascontiguousarray(graph.degrees, dtype=np.int32)
+        st = L.bang_index_create(self.device, _lib.ptr(cds), self.n, m, _lib.ptr(cb), _lib.ptr(sizes),
+                                 self.dim, _lib.ptr(adj), _lib.ptr(deg), adj.shape[1], graph.medoid,
+                                 _lib.ptr(vec), _VEC_CODE[vec.dtype], placement, ctypes.byref(handle))
+        _lib.check(st, "bang_index_create")
+        self.handle = handle
+        self.m = m
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            _lib.lib().bang_index_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def search(self, queries: np.ndarray, k: int, t: int, bloom_entries: int, flags: int):
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        nq = q.shape[0]
+        ids = np.empty((nq, k), np.int32)
+        dists = np.empty((nq, k), np.float32)
+        iters = np.empty(nq, np.int32)
+        conv = np.empty(nq, np.uint8)
+        short = np.empty(nq, np.uint8)
+        wall = np.empty(nq, np.float64)
+        offs = np.empty(nq + 1, np.int64)
+        L = _lib.lib()
+        st = L.bang_search(self.handle, _lib.ptr(q), nq, k, t, int(bloom_entries), flags, _lib.ptr(ids),
+                           _lib.ptr(dists), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(short),
+                           _lib.ptr(wall), _lib.ptr(offs), None, 0)
+        _lib.check(st, "bang_search")
+        flat = np.empty(int(offs[-1]), np.int32)
+        _lib.check(L.bang_last_visit_logs(self.handle, _lib.ptr(flat), flat.size), "bang_last_visit_logs")
+        return ids, dists, iters, conv.astype(bool), short.astype(bool), wall, offs, flat
+
+    def stats(self) -> dict:
+        s = _lib.SearchStats()
+        _lib.check(_lib.lib().bang_last_search_stats(self.handle, ctypes.byref(s)))
+        return s.as_dict()
+
+
+def exact_sq_dists(points, queries) -> np.ndarray:
+    """engine.py:48-51 on the GPU: row-paired squared L2, f64 sums -> f32."""
+    p = as_engine_rows(check_matrix(points, "points"))
+    q = as_float32_rows(np.ascontiguousarray(np.broadcast_to(queries, p.shape), dtype=np.float32))
+    if p.shape[0] == 0:
+        return np.zeros(0, np.float32)
+    dp, dq = _dev.to_dev(p), _dev.to_dev(q)
+    out = _dev.empty((p.shape[0],), np.float32)
+    _lib.check(_lib.lib().bang_exact_sq_dists_device(_lib.ptr(dp), _VEC_CODE[p.dtype], p.shape[1],
+                                                     _lib.ptr(dq), p.shape[0], _lib.ptr(out),
+                                                     _lib.stream_ptr(_dev.stream())), "exact_sq_dists")
+    return _dev.to_host(out)
+
+
+def rerank(candidate_ids, candidate_vectors, query, k: int):
+    """engine.py:273-292: exact-distance ordering of one query's candidates."""
+    ids = np.asarray(candidate_ids, dtype=np.int64)
+    vecs = check_matrix(candidate_vectors, "candidate_vectors")
+    q = as_float32_rows(np.asarray(query, dtype=np.float32).reshape(1, -1))[0]
+    if ids.size != vecs.shape[0]:
+        raise ParameterError("one vector per candidate id required")
+    if ids.size == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.float32), k > 0
+    dists = exact_sq_dists(vecs, np.broadcast_to(q, (vecs.shape[0], q.size)))
+    keys = np.full((1, _next_pow2(ids.size)), SENTINEL, dtype=np.uint64)
+    keys[0, :ids.size] = pack_keys(dists, ids)
+    ordered = merge_sort_rows(keys)[0, :min(k, ids.size)]
+    d_out, i_out = unpack_keys(ordered)
+    return i_out, d_out, ids.size < k
+
+
+class GraphSearcher(BaseEstimator):
+    """Batched approximate k-NN search over a graph index (engine.py:335-460).
+
+    Same constructor parameters, defaults, checks and outputs as the
+    reference.  ``mode`` picks where the graph lives: "in_memory" (HBM),
+    "pipelined" (pinned, mapped host memory read over PCIe with the next
+    hop prefetched) or "exact_distance" (exact f64->f32 scoring, no codes,
+    no re-rank).  ``threads`` is accepted and ignored (the GPU result does
+    not depend on it, as the reference's does not).
+    """
+
+    def __init__(self, k: int = 10, t: int = 152, mode: str = "pipelined",
+                 bloom_entries: int = DEFAULT_ENTRIES, batch_size: int = 10_000,
+                 rerank: bool = True, degree_bound: int = 64,
+                 build_worklist: int = 200, sigma: float = 1.2, m: int = 74,
+                 pq_iters: int = 25, seed: int = 0, threads: int | None = None,
+                 debug_checks: bool = False):
+        self.k = k
+        self.t = t
+        self.mode = mode
+        self.bloom_entries = bloom_entries
+        self.batch_size = batch_size
+        self.rerank = rerank
+        self.degree_bound = degree_bound
+        self.build_worklist = build_worklist
+        self.sigma = sigma
+        self.m = m
+        self.pq_iters = pq_iters
+        self.seed = seed
+        self.threads = threads
+        self.debug_checks = debug_checks
+
+    def _check_params(self):
+        """engine.py:368-375."""
+        check_positive("k", self.k)
+        if self.t < self.k:
+            raise ParameterError(f"t={self.t} must be >= k={self.k}")
+        if self.mode not in MODES:
+            raise ParameterError(f"mode must be one of {MODES}, got {self.mode!r}")
+        check_positive("bloom_entries", self.bloom_entries)
+        check_positive("batch_size", self.batch_size)
+
+    def fit(self, X, y=None, graph: GraphIndex | None = None, codebook: PQCodebook | None = None,
+            codes: CompressedVectors | None = None) -> "GraphSearcher":
+        """engine.py:377-407: attach (or build) the artifacts and upload them."""
+        self._check_params()
+        data = getattr(X, "data", X)
+        base = as_engine_rows(check_matrix(data, "X"))
+        if graph is None:
+            from .tools.graph_build import build_graph
+            graph = build_graph(base, degree_bound=self.degree_bound, build_worklist=self.build_worklist,
+                                sigma=self.sigma, seed=self.seed)
+        if graph.node_count != base.shape[0]:
+            raise ParameterError("graph node count does not match the base set")
+        if self.mode != "exact_distance":
+            if codebook is None:
+                from .tools.pq_train import train_codebook
+                codebook = train_codebook(base, m=self.m, iters=self.pq_iters, seed=self.seed)
+            if codebook.dim != base.shape[1]:
+                raise ParameterError("codebook dimension does not match the base set")
+            if codes is None:
+                from .tools.pq_train import encode
+                codes = encode(base, codebook)
+            if codes.count != base.shape[0] or codes.m != codebook.m:
+                raise ParameterError("compressed vectors do not match base/codebook")
+        else:
+            codebook, codes = None, None
+        placement = _lib.GRAPH_HOST_MAPPED if self.mode == "pipelined" else _lib.GRAPH_HBM
+        old = getattr(self, "index_", None)
+        if old is not None:
+            old.close()
+        self.index_ = DeviceIndex(graph, base, codebook, codes, placement)
+        self.host_ = IndexHost(graph, base)
+        self.graph_ = graph
+        self.codebook_ = codebook
+        self.codes_ = codes
+        self.engine_vectors_ = base if self.mode != "pipelined" else None
+        return self
+
+    def _flags(self) -> int:
+        flags = 0
+        if self.rerank:
+            flags |= _lib.RERANK
+        if self.debug_checks:
+            flags |= _lib.DEBUG_CHECKS
+        if self.mode == "exact_distance":
+            flags |= _lib.EXACT_DISTANCE
+        return flags
+
+    def search(self, queries, k: int | None = None) -> SearchResult:
+        """engine.py:409-452; deterministic for fixed inputs and params."""
+        if not hasattr(self, "host_"):
+            raise ParameterError("GraphSearcher is not fitted")
+        k = self.k if k is None else int(k)
+        if k < 1 or k > self.t:
+            raise ParameterError(f"k={k} must be in [1, t={self.t}]")
+        data = getattr(queries, "data", queries)
+        q = as_float32_rows(check_matrix(data, "queries"))
+        nq = q.shape[0]
+        if nq == 0:
+            return SearchResult(np.zeros((0, k), np.int32), np.zeros((0, k), np.float32),
+                                np.zeros(0, np.int32), np.zeros(0, bool), np.zeros(0, np.float64), 0.0,
+                                np.zeros(0, bool), [])
+        if q.shape[1] != self.host_.vectors.shape[1]:
+            raise ParameterError("query dimension does not match the base set")
+        parts = []
+        elapsed = 0.0
+        flags = self._flags()
+        for lo in range(0, nq, self.batch_size):
+            hi = min(nq, lo + self.batch_size)
+            t0 = time.perf_counter()
+            parts.append(self.index_.search(q[lo:hi], k, self.t, self.bloom_entries, flags))
+            elapsed += time.perf_counter() - t0
+        logs = []
+        for p in parts:
+            offs, flat = p[6], p[7].astype(np.int64)
+            logs.extend(np.split(flat, offs[1:-1]))
+        return SearchResult(
+            ids=np.concatenate([p[0] for p in parts]),
+            dists=np.concatenate([p[1] for p in parts]),
+            iterations=np.concatenate([p[2] for p in parts]),
+            converged=np.concatenate([p[3] for p in parts]),
+            wall_times=np.concatenate([p[5] for p in parts]),
+            elapsed=elapsed,
+            short=np.concatenate([p[4] for p in parts]),
+            visit_logs=logs)
+
+    def kneighbors(self, queries, n_neighbors: int | None = None, return_distance: bool = True):
+        """scikit-learn style accessor over :meth:`search` (engine.py:454-460)."""
+        result = self.search(queries, k=n_neighbors)
+        if return_distance:
+            return result.dists, result.ids
+        return result.ids
+
+    def last_stats(self) -> dict:
+        """Counters of the last batch (iterations, probes, ADC pairs, kernel ms)."""
+        return self.index_.stats()
