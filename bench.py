@@ -1,0 +1,351 @@
+"""Benchmark of the B200 batched graph search (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config C2]
+
+One "step" = one batched search of the config's query batch (10K queries at
+C2) at the smallest worklist size t whose recall@10 >= 0.9 (chosen by a
+sweep before timing).  Reported:
+  value  QPS with queries/outputs resident in HBM (bang_search_device), the
+         sum of per-step CUDA-event times on the launching stream, L2 flushed
+         (256 MiB memset) between steps outside the events, max over ranks;
+  e2e    QPS through the public API GraphSearcher.search with the queries in
+         pinned host memory (H2D, search, D2H of ids/dists/iterations/short/
+         visit logs inside the timed region);
+  roofline  the fused search kernel's algorithmic HBM bytes / its event time;
+  cpu_baseline  the CPU oracle (oracle/, a C port of the reference path, all
+         host threads) on a bounded sample of the same queries.
+Multi-GPU (torchrun): each rank searches its own 10K-query shard against a
+replicated index (weak scaling); no collective on the search path.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_SWEEP = (10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 128, 160, 200)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6 for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def recall(ids, gt, k=10):
+    from paper_2401_11324_b200.tools.groundtruth import recall_at_k
+    return recall_at_k(ids, gt, k)
+
+
+def cpu_oracle_qps(art, t, k, bloom, budget_s=12.0, max_q=None):
+    """CPU oracle (C port of the reference path, OpenMP over queries) on a
+    bounded sample of the benchmark queries."""
+    from oracle import oracle as O
+    O.build()
+    cores = os.cpu_count() or 1
+    q = art["queries"]
+    g = art["graph"]
+    cb = art["codebook"]
+    kw = dict(centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=art["codes"].codes,
+              adjacency=g.adjacency, degrees=g.degrees, medoid=g.medoid, vectors=art["base"], k=k, t=t,
+              bloom_entries=bloom, threads=cores)
+    probe = min(q.shape[0], 8 * cores)
+    t0 = time.perf_counter()
+    O.search(q[:probe], **kw)
+    per_q = (time.perf_counter() - t0) / probe
+    n = int(min(q.shape[0], max(probe, budget_s / max(per_q, 1e-9))))
+    if max_q:
+        n = min(n, max_q)
+    t0 = time.perf_counter()
+    res = O.search(q[:n], **kw)
+    dt = time.perf_counter() - t0
+    return dict(value=n / dt, unit="queries/s", cores=cores, kind="port", seconds=dt, queries=n,
+                sample=f"first {n} of the {q.shape[0]} benchmark queries, t={t}, k={k}, all {cores} host "
+                       f"threads (OpenMP over queries)"), res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--config", default=os.environ.get("BANG_BENCH_CONFIG", "C2"))
+    ap.add_argument("--t", type=int, default=0, help="fixed worklist size (default: recall sweep)")
+    ap.add_argument("--target-recall", type=float, default=0.9)
+    ap.add_argument("--bloom", type=int, default=399_887)
+    ap.add_argument("--cache", default=os.environ.get("BANG_BENCH_CACHE", "/tmp/bang_bench_cache"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem", "table"))
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    k = 10
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local) if torch.cuda.is_available() else None
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
+                                init_method="env://")
+    if args.impl == "reference" and rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    from paper_2401_11324_b200 import GraphSearcher, _lib, set_device
+    from paper_2401_11324_b200.tools.bench_data import CONFIGS, build_artifacts
+    set_device(local)
+    nq = CONFIGS[args.config][1]
+    # each rank owns its own nq-query shard (weak scaling)
+    art = build_artifacts(args.config, seed=0, nq_total=nq * world, cache_dir=args.cache or None, log=log)
+    lo, hi = rank * nq, (rank + 1) * nq
+    shard = dict(art)
+    shard["queries"] = art["queries"][lo:hi]
+    shard["gt_ids"] = art["gt_ids"][lo:hi]
+    meta = art["meta"]
+    searcher = GraphSearcher(k=k, t=max(T_SWEEP), mode="in_memory", bloom_entries=args.bloom,
+                             batch_size=nq)
+    searcher.fit(art["base"], graph=art["graph"], codebook=art["codebook"], codes=art["codes"])
+
+    # ---- worklist size at recall >= target (the metric's operating point)
+    sweep = []
+    t_sel = args.t
+    if not t_sel:
+        for t in T_SWEEP:
+            searcher.t = t
+            res = searcher.search(shard["queries"])
+            r = recall(res.ids, shard["gt_ids"], k)
+            sweep.append({"t": t, "recall": round(r, 4), "mean_iters": float(res.iterations.mean())})
+            if r >= args.target_recall:
+                t_sel = t
+                break
+        if not t_sel:
+            t_sel = T_SWEEP[-1]
+    if world > 1:
+        tt = torch.tensor([t_sel], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_sel = int(tt.item())
+    searcher.t = t_sel
+    log(f"[bench] rank {rank}: t={t_sel} sweep={sweep}")
+
+    config = {"workload": args.config, "desc": meta["desc"], "n": meta["n"], "dim": meta["dim"],
+              "vectors": meta["dtype"], "R": meta["R"], "m": meta["m"], "k": k, "t": t_sel,
+              "queries_per_gpu": nq, "bloom_entries": args.bloom, "mode": "in_memory",
+              "graph": "GPU kNN(2R) + RobustPrune(1.2) + reverse edges (tools/graph_build.py)",
+              "l2": "flushed between steps (256 MiB memset outside the step events)",
+              "parallelism": f"query-sharded x{world}, index replicated, no collective"}
+
+    if args.impl == "reference":
+        cpu, res = cpu_oracle_qps(art, t_sel, k, args.bloom, budget_s=max(5.0, 60.0 / max(1, args.steps)))
+        steps = []
+        for _ in range(args.steps):
+            c, _ = cpu_oracle_qps(art, t_sel, k, args.bloom, budget_s=max(5.0, 60.0 / max(1, args.steps)),
+                                  max_q=cpu["queries"])
+            steps.append(c["value"])
+        v = float(np.mean(steps))
+        out = {"impl": "reference", "metric": f"queries/sec at recall@10>=0.9 ({args.config})",
+               "value": round(v, 2), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(1000.0 * cpu["queries"] / v, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+               "data": "synthetic (seeded Gaussian mixture)", "config": config,
+               "cpu_baseline": {"value": round(v, 2), "unit": "queries/s", "cores": cpu["cores"],
+                                "kind": "port", "sample": cpu["sample"]},
+               "e2e": {"value": round(v, 2), "unit": "queries/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- device-resident timing (value)
+    flags = _lib.RERANK | ({"auto": 0, "smem": _lib.TABLE_SMEM, "table": _lib.TABLE_GLOBAL}[args.variant])
+    dev = torch.device("cuda", local)
+    dq = torch.from_numpy(np.ascontiguousarray(shard["queries"], np.float32)).to(dev)
+    d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+    d_it = torch.empty((nq,), dtype=torch.int32, device=dev)
+    d_short = torch.empty((nq,), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    h = searcher.index_.handle
+    L = _lib.lib()
+
+    def device_step():
+        _lib.check(L.bang_search_device(h, _lib.ptr(dq), nq, k, t_sel, args.bloom, flags, _lib.ptr(d_ids),
+                                        _lib.ptr(d_dists), _lib.ptr(d_it), _lib.ptr(d_short),
+                                        _lib.stream_ptr(stream)), "bang_search_device")
+
+    warm = 1 if args.profile else max(3, args.warmup)
+    steps = 1 if args.profile else args.steps
+    for _ in range(warm):
+        flush.zero_()
+        device_step()
+        _lib.check(L.bang_sync_status(h))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    kern_ms, stats = [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            device_step()
+            ev[i][1].record(stream)
+            _lib.check(L.bang_sync_status(h))  # synchronises; outside the events
+            st = searcher.index_.stats()
+            kern_ms.append(st["kernel_ms"])
+            stats.append(st)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms = float(tmax.item())
+    value = nq * world * steps / (total_ms / 1000.0)
+    ids_dev = d_ids.cpu().numpy()
+    rec_dev = recall(ids_dev, shard["gt_ids"], k)
+
+    if args.profile:
+        log(f"[bench] profile step: {step_ms} ms, stats {stats[-1]}")
+        return
+
+    # ---- end to end through the public API (pinned host queries)
+    qpin = torch.empty(shard["queries"].shape, dtype=torch.float32, pin_memory=True)
+    qpin.copy_(torch.from_numpy(np.ascontiguousarray(shard["queries"], np.float32)))
+    qhost = qpin.numpy()
+    e2e_s = []
+    res = None
+    for i in range(warm + steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = searcher.search(qhost)
+        dt = time.perf_counter() - t0
+        if i >= warm:
+            e2e_s.append(dt)
+    e2e_tot = torch.tensor([float(sum(e2e_s))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
+    e2e_value = nq * world * steps / float(e2e_tot.item())
+    rec_e2e = recall(res.ids, shard["gt_ids"], k)
+    assert np.array_equal(res.ids, ids_dev), "device-resident and end-to-end paths disagree"
+    h2d = nq * meta["dim"] * 4
+    d2h = nq * (k * 8 + 4 + 1 + 1 + 8 + 8) + 8 + 4 * int(res.iterations.sum())
+
+    # ---- roofline of the fused search kernel
+    peak, peak_kind = measured_peaks()
+    s_last = stats[-1]
+    avg_kern_ms = float(np.mean(kern_ms))
+    achieved = s_last["algorithmic_bytes"] / (avg_kern_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(args.config)
+            if tr and tr.get("t") == t_sel:
+                traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "kernel": "bang::search_kernel", "kernel_ms": round(avg_kern_ms, 4),
+                "algorithmic_bytes": s_last["algorithmic_bytes"],
+                "adc_bytes": s_last["adc_bytes"],
+                "adc_gbs": round(s_last["adc_bytes"] / (avg_kern_ms / 1000.0) / 1e9, 1)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu, _ = cpu_oracle_qps(art, t_sel, k, args.bloom)
+        cpu = {kk: (round(v, 2) if isinstance(v, float) else v) for kk, v in cpu.items()}
+
+    out = {"metric": f"queries/sec at recall@10>=0.9 ({args.config})", "value": round(value, 1),
+           "unit": "queries/s", "n_gpus": world, "steps": steps, "warmup": warm,
+           "ms_per_step": round(total_ms / steps, 4), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32 (u8 codes; f32 ADC sums, f64 re-rank)",
+           "data": "synthetic (seeded Gaussian mixture, random-init artifacts built on GPU)",
+           "config": config, "recall_at_10": round(rec_e2e, 4), "recall_device_path": round(rec_dev, 4),
+           "t_sweep": sweep,
+           "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": round(1000 * float(e2e_tot.item()) / steps, 3)},
+           "gpu_launches": 2 * steps + (1 if s_last["adc_variant"] == 1 else 0) * steps,
+           "roofline": roofline, "cpu_baseline": cpu,
+           "clocks": clk.summary(),
+           "search_stats": {kk: s_last[kk] for kk in ("iterations", "probes", "fresh", "rerank_cands", "slots",
+                                                      "warps_per_cta", "ctas", "adc_variant", "retries")},
+           "step_ms": [round(x, 4) for x in step_ms]}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
