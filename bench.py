@@ -231,7 +231,10 @@ def main():
     d_it = torch.empty((nq,), dtype=torch.int32, device=dev)
     d_short = torch.empty((nq,), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the legacy default stream's handle is 0, which the
+    # C-ABI reads as "the handle's own stream"
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     h = searcher.index_.handle
     L = _lib.lib()
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass
 
 import numpy as np
@@ -37,6 +38,40 @@ except ImportError:  # pragma: no cover
 MODES = ("pipelined", "in_memory", "exact_distance")
 _VEC_CODE = {np.dtype(np.float32): _lib.VEC_F32, np.dtype(np.uint8): _lib.VEC_U8,
              np.dtype(np.int8): _lib.VEC_I8}
+
+
+class VisitLogs(Sequence):
+    """Per-query visit logs as a read-only list of int64 arrays, backed by one
+    CSR buffer (offsets + flat ids) so a 10K-query batch costs no Python
+    loop; ``logs[i]`` is query i's expanded ids in visit order."""
+
+    def __init__(self, parts):
+        self._offs = []
+        self._flat = []
+        self._base = [0]
+        for offs, flat in parts:
+            self._offs.append(np.asarray(offs, np.int64))
+            self._flat.append(np.asarray(flat).astype(np.int64, copy=False))
+            self._base.append(self._base[-1] + len(offs) - 1)
+
+    def __len__(self):
+        return self._base[-1]
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        n = len(self)
+        if i < 0:
+            i += n
+        if not 0 <= i < n:
+            raise IndexError("visit log index out of range")
+        p = int(np.searchsorted(self._base, i, side="right")) - 1
+        j = i - self._base[p]
+        offs = self._offs[p]
+        return self._flat[p][offs[j]:offs[j + 1]]
+
+    def __eq__(self, other):
+        return len(self) == len(other) and all(np.array_equal(a, b) for a, b in zip(self, other))
 
 
 @dataclass
@@ -277,10 +312,7 @@ class GraphSearcher(BaseEstimator):
             t0 = time.perf_counter()
             parts.append(self.index_.search(q[lo:hi], k, self.t, self.bloom_entries, flags))
             elapsed += time.perf_counter() - t0
-        logs = []
-        for p in parts:
-            offs, flat = p[6], p[7].astype(np.int64)
-            logs.extend(np.split(flat, offs[1:-1]))
+        logs = VisitLogs([(p[6], p[7]) for p in parts])
         return SearchResult(
             ids=np.concatenate([p[0] for p in parts]),
             dists=np.concatenate([p[1] for p in parts]),
