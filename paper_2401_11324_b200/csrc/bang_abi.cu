@@ -124,7 +124,8 @@ struct Plan {
     int npl = 2, sub = 0, mv = 0;
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
-    int off_q, off_wl, off_sk, off_fid, off_vis;
+    int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum;
+    int sum_words = 0;
     int64_t bloom_stride = 0;
 };
 
@@ -151,13 +152,22 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     if (ix->R > 128) return fail(BANG_E_PARAM, "degree bound R=%d exceeds 128", ix->R);
     const bool exact = flags & BANG_EXACT_DISTANCE;
     const int64_t cb_bytes = (int64_t)256 * ix->dim * 4;
-    const int per_warp_q = (int)align_up((int64_t)ix->dim * 4, 16);
+    // per-warp shared memory: query, worklist keys, sorted/unsorted new
+    // keys, fresh ids, partial ADC sums, alive list, visited flags, Bloom
+    // summary (one bit per u32 filter word)
+    const int rpad = pl.npl * 32;
+    pl.bloom_stride = align_up(ceil_div(z, 32), 4);
+    pl.sum_words = (int)ceil_div(pl.bloom_stride, 32);
     pl.off_q = 0;
-    pl.off_wl = per_warp_q;
+    pl.off_wl = (int)align_up((int64_t)ix->dim * 4, 16);
     pl.off_sk = pl.off_wl + (int)align_up((int64_t)t * 8, 16);
-    pl.off_fid = pl.off_sk + (int)align_up((int64_t)pl.npl * 32 * 8, 16);
-    pl.off_vis = pl.off_fid + (int)align_up((int64_t)pl.npl * 32 * 4, 16);
-    pl.per_warp = pl.off_vis + (int)align_up(t, 16);
+    pl.off_nk = pl.off_sk + (int)align_up((int64_t)rpad * 8, 16);
+    pl.off_fid = pl.off_nk + (int)align_up((int64_t)rpad * 8, 16);
+    pl.off_acc = pl.off_fid + (int)align_up((int64_t)rpad * 4, 16);
+    pl.off_alive = pl.off_acc + (int)align_up((int64_t)rpad * 4, 16);
+    pl.off_vis = pl.off_alive + (int)align_up(rpad, 16);
+    pl.off_sum = pl.off_vis + (int)align_up(t, 16);
+    pl.per_warp = pl.off_sum + (int)align_up((int64_t)pl.sum_words * 4, 16);
     const int mv = (ix->m % 16 == 0 && ix->m / 16 >= 2 && ix->m / 16 <= 3) ? ix->m / 16 : 0;
     if (exact) {
         pl.variant = kAdcExact;
@@ -200,7 +210,6 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     }
     pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, ceil_div(nq, pl.warps)));
     pl.slots = pl.ctas * pl.warps;
-    pl.bloom_stride = align_up(ceil_div(z, 32), 4);
     return BANG_OK;
 }
 
@@ -255,8 +264,13 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_q = pl.off_q;
     p.off_wl = pl.off_wl;
     p.off_sk = pl.off_sk;
+    p.off_nk = pl.off_nk;
     p.off_fid = pl.off_fid;
+    p.off_acc = pl.off_acc;
+    p.off_alive = pl.off_alive;
     p.off_vis = pl.off_vis;
+    p.off_sum = pl.off_sum;
+    p.sum_words = pl.sum_words;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);
@@ -772,17 +786,14 @@ bang_status bang_worklist_update_device(uint64_t *d_wl_keys, uint8_t *d_wl_vis, 
     if (w < 0 || w > 128) return fail(BANG_E_PARAM, "new-key width %d outside [0, 128]", w);
     if (rows == 0) return BANG_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int npl = w <= 32 ? 1 : (w <= 64 ? 2 : 4);
-    const int per_warp = (int)(align_up(8LL * t, 16) + align_up(8LL * npl * 32, 16) + align_up(t, 16));
+    const int per_warp = (int)(align_up(8LL * t, 16) + 2 * align_up(8LL * w, 16) + align_up(t, 16));
     const int warps = 4;
     const size_t smem = (size_t)per_warp * warps;
+    if (smem > 227 * 1024) return fail(BANG_E_PARAM, "t=%d too large for the worklist kernel", t);
     const unsigned grid = (unsigned)ceil_div(rows, warps);
-#define BANG_WL(N)                                                                                            \
-    CU(cudaFuncSetAttribute(worklist_update_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    worklist_update_kernel<N><<<grid, warps * 32, smem, st>>>(d_wl_keys, d_wl_vis, rows, t, d_new_keys, w,   \
-                                                               d_winner, d_done);
-    if (npl == 1) { BANG_WL(1) } else if (npl == 2) { BANG_WL(2) } else { BANG_WL(4) }
-#undef BANG_WL
+    CU(cudaFuncSetAttribute(worklist_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    worklist_update_kernel<<<grid, warps * 32, smem, st>>>(d_wl_keys, d_wl_vis, rows, t, d_new_keys, w, d_winner,
+                                                           d_done);
     CU(cudaGetLastError());
     return BANG_OK;
 }

@@ -76,89 +76,187 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
 // One warp test-and-sets one row's probes (up to NPL*32 ids, probe i lives
 // in lane i%32, register i/32) against one filter of u32 words.
 // Semantics = sequential test-and-set in probe order (bloom.py:124-163):
-//  1. every probe tests the PRE-state (two L2 loads, issued together);
-//  2. fresh probes set their bits with fetch-or atomics; a bit that a
-//     different fresh probe of this row set first shows up in the returned
-//     old word while it was clear in the pre-state -- exactly the in-row
-//     slot sharing that bloom.py:134-158 detects;
-//  3. on any such collision (rare: ~0.3% of rows at z = 399,887) the
-//     touched words are restored to the pre-state and the row is replayed
-//     in order by lane 0 (bloom.py:110-122) -- bit-exact, unlike the
-//     paper's tolerated race.
-// The filter is read through L2 (ld.global.cg) because it is written by
-// atomics performed at L2 during the same kernel.
+//  1. every probe tests the PRE-state (two L2 loads issued together);
+//  2. fresh probes set their bits with fetch-or atomics; a bit that another
+//     fresh probe of this row set first shows up in the returned old word
+//     while it was clear in the pre-state -- exactly the in-row slot
+//     sharing that bloom.py:134-158 detects;
+//  3. on such a collision (rare: ~0.3% of rows at z = 399,887) the touched
+//     words are restored to the pre-state and lane 0 replays the row in
+//     order (bloom.py:110-122) -- bit-exact, unlike the paper's tolerated
+//     race.
+// Phase 2 is split (bloom_issue / bloom_resolve) so the atomics' round trip
+// overlaps the ADC of the fresh neighbours.
+//
+// Optional per-warp summary (s_sum != nullptr; the fused search kernel):
+// one smem bit per filter word, set when the word is first written by the
+// current query.  A word whose summary bit is clear holds garbage from an
+// earlier query and is read as 0 without touching memory, so the 50 KB
+// filter never needs clearing and only words this query wrote are ever
+// read (most probes then cost no load at all).  The filter state it
+// represents is identical: bit p is set <=> summary(p>>5) && word(p>>5) has p.
+// Filters are read through L2 (ld.global.cg): they are written by atomics
+// performed at L2 during the same kernel.
 template <int NPL>
-__device__ __forceinline__ void bloom_test_and_set(uint32_t *__restrict__ bits,
-                                                   const BloomGeom &g,
-                                                   const uint32_t (&ids)[NPL], int cnt,
-                                                   bool (&fresh)[NPL]) {
+struct BloomRow {
+    uint32_t p1[NPL], p2[NPL], w1[NPL], w2[NPL], o1[NPL], o2[NPL];
+    bool i1[NPL], i2[NPL];  // word was initialised before this row (summary)
+    bool fresh[NPL];
+};
+
+__device__ __forceinline__ bool sum_get(const uint32_t *s_sum, uint32_t w) {
+    return (s_sum[w >> 5] >> (w & 31)) & 1u;
+}
+__device__ __forceinline__ void sum_set(uint32_t *s_sum, uint32_t w) {
+    atomicOr(s_sum + (w >> 5), 1u << (w & 31));
+}
+
+template <int NPL>
+__device__ __forceinline__ void bloom_issue(uint32_t *__restrict__ bits, uint32_t *s_sum,
+                                            const BloomGeom &g, const uint32_t (&ids)[NPL],
+                                            int cnt, BloomRow<NPL> &b) {
     const int lane = (int)lane_id();
-    uint32_t p1[NPL], p2[NPL], w1[NPL], w2[NPL];
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
-        fresh[k] = false;
-        p1[k] = p2[k] = w1[k] = w2[k] = 0;
+        b.fresh[k] = false;
+        b.p1[k] = b.p2[k] = b.w1[k] = b.w2[k] = b.o1[k] = b.o2[k] = 0;
+        b.i1[k] = b.i2[k] = true;
         if (lane + 32 * k < cnt) {
-            p1[k] = mod_z(fnv1a(ids[k], kFnvOffset), g);
-            p2[k] = mod_z(fnv1a(ids[k], kFnvOffsetH2), g);
-            w1[k] = __ldcg(bits + (p1[k] >> 5));
-            w2[k] = __ldcg(bits + (p2[k] >> 5));
+            b.p1[k] = mod_z(fnv1a(ids[k], kFnvOffset), g);
+            b.p2[k] = mod_z(fnv1a(ids[k], kFnvOffsetH2), g);
+            if (s_sum) {
+                b.i1[k] = sum_get(s_sum, b.p1[k] >> 5);
+                b.i2[k] = sum_get(s_sum, b.p2[k] >> 5);
+            }
+            if (b.i1[k]) b.w1[k] = __ldcg(bits + (b.p1[k] >> 5));
+            if (b.i2[k]) b.w2[k] = __ldcg(bits + (b.p2[k] >> 5));
         }
     }
 #pragma unroll
     for (int k = 0; k < NPL; ++k)
         if (lane + 32 * k < cnt)
-            fresh[k] = !(((w1[k] >> (p1[k] & 31)) & 1u) && ((w2[k] >> (p2[k] & 31)) & 1u));
-    __syncwarp();  // every pre-state load has landed before any atomic
+            b.fresh[k] = !(((b.w1[k] >> (b.p1[k] & 31)) & 1u) && ((b.w2[k] >> (b.p2[k] & 31)) & 1u));
+    __syncwarp();  // every pre-state load has landed before any write below
+    if (s_sum) {
+        // words first written by this query: zero them and mark the summary
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < NPL; ++k) {
+            if (b.fresh[k] && !b.i1[k]) {
+                __stcg(bits + (b.p1[k] >> 5), 0u);
+                sum_set(s_sum, b.p1[k] >> 5);
+                any = true;
+            }
+            if (b.fresh[k] && !b.i2[k]) {
+                __stcg(bits + (b.p2[k] >> 5), 0u);
+                sum_set(s_sum, b.p2[k] >> 5);
+                any = true;
+            }
+        }
+        if (__any_sync(kFull, any)) {
+            __threadfence_block();
+            __syncwarp();  // the zeroing stores are ordered before the atomics
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        if (b.fresh[k]) {
+            b.o1[k] = atomicOr(bits + (b.p1[k] >> 5), 1u << (b.p1[k] & 31));
+            if (b.p2[k] != b.p1[k]) b.o2[k] = atomicOr(bits + (b.p2[k] >> 5), 1u << (b.p2[k] & 31));
+        }
+    }
+}
+
+// Checks the atomics' old words; on an in-row collision restores the
+// pre-state and replays the row sequentially.  Returns true (warp-uniform)
+// when the fresh set was recomputed.
+template <int NPL>
+__device__ __forceinline__ bool bloom_resolve(uint32_t *__restrict__ bits, uint32_t *s_sum,
+                                              const BloomGeom &g, const uint32_t (&ids)[NPL],
+                                              int cnt, BloomRow<NPL> &b) {
+    const int lane = (int)lane_id();
     bool coll = false;
 #pragma unroll
     for (int k = 0; k < NPL; ++k) {
-        if (fresh[k]) {
-            const uint32_t b1 = 1u << (p1[k] & 31);
-            const uint32_t o1 = atomicOr(bits + (p1[k] >> 5), b1);
-            coll |= (o1 & b1) && !(w1[k] & b1);
-            if (p2[k] != p1[k]) {
-                const uint32_t b2 = 1u << (p2[k] & 31);
-                const uint32_t o2 = atomicOr(bits + (p2[k] >> 5), b2);
-                coll |= (o2 & b2) && !(w2[k] & b2);
+        if (b.fresh[k]) {
+            const uint32_t b1 = 1u << (b.p1[k] & 31);
+            coll |= (b.o1[k] & b1) && !(b.w1[k] & b1);
+            if (b.p2[k] != b.p1[k]) {
+                const uint32_t b2 = 1u << (b.p2[k] & 31);
+                coll |= (b.o2[k] & b2) && !(b.w2[k] & b2);
             }
         }
     }
-    if (__any_sync(kFull, coll)) {
-        // restore the pre-state of every word a fresh probe touched
-#pragma unroll
-        for (int k = 0; k < NPL; ++k) {
-            if (fresh[k]) {
-                __stcg(bits + (p1[k] >> 5), w1[k]);
-                __stcg(bits + (p2[k] >> 5), w2[k]);
-            }
-        }
-        __threadfence_block();
+    if (!__any_sync(kFull, coll)) {
         __syncwarp();
-        uint32_t mask[NPL];
+        return false;
+    }
+    // restore the pre-state of every word a fresh probe touched
 #pragma unroll
-        for (int k = 0; k < NPL; ++k) {
-            mask[k] = 0;
-            const int n = min(32, cnt - 32 * k);
-            for (int j = 0; j < n; ++j) {
-                const uint32_t id = __shfl_sync(kFull, ids[k], j);
-                if (lane == 0) {
-                    const uint32_t q1 = mod_z(fnv1a(id, kFnvOffset), g);
-                    const uint32_t q2 = mod_z(fnv1a(id, kFnvOffsetH2), g);
-                    const uint32_t b1 = 1u << (q1 & 31), b2 = 1u << (q2 & 31);
-                    const bool hit = (__ldcg(bits + (q1 >> 5)) & b1) && (__ldcg(bits + (q2 >> 5)) & b2);
-                    if (!hit) {
-                        atomicOr(bits + (q1 >> 5), b1);
-                        atomicOr(bits + (q2 >> 5), b2);
-                        mask[k] |= 1u << j;
+    for (int k = 0; k < NPL; ++k) {
+        if (b.fresh[k]) {
+            if (b.i1[k]) __stcg(bits + (b.p1[k] >> 5), b.w1[k]);
+            if (b.i2[k]) __stcg(bits + (b.p2[k] >> 5), b.w2[k]);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        if (b.fresh[k] && s_sum) {
+            if (!b.i1[k]) atomicAnd(s_sum + ((b.p1[k] >> 5) >> 5), ~(1u << ((b.p1[k] >> 5) & 31)));
+            if (!b.i2[k]) atomicAnd(s_sum + ((b.p2[k] >> 5) >> 5), ~(1u << ((b.p2[k] >> 5) & 31)));
+        }
+    }
+    __threadfence_block();
+    __syncwarp();
+    // sequential replay in appearance order (lane 0)
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        uint32_t mask = 0;
+        const int n = min(32, cnt - 32 * k);
+        for (int j = 0; j < n; ++j) {
+            const uint32_t id = __shfl_sync(kFull, ids[k], j);
+            if (lane == 0) {
+                const uint32_t q[2] = {mod_z(fnv1a(id, kFnvOffset), g), mod_z(fnv1a(id, kFnvOffsetH2), g)};
+                bool hit = true;
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t w = q[h] >> 5;
+                    const bool init = !s_sum || sum_get(s_sum, w);
+                    hit = hit && init && ((__ldcg(bits + w) >> (q[h] & 31)) & 1u);
+                }
+                if (!hit) {
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t w = q[h] >> 5;
+                        if (s_sum && !sum_get(s_sum, w)) {
+                            __stcg(bits + w, 1u << (q[h] & 31));
+                            s_sum[w >> 5] |= 1u << (w & 31);
+                        } else {
+                            atomicOr(bits + w, 1u << (q[h] & 31));
+                        }
                     }
+                    mask |= 1u << j;
                 }
             }
-            mask[k] = __shfl_sync(kFull, mask[k], 0);
-            fresh[k] = (mask[k] >> lane) & 1u;
         }
+        mask = __shfl_sync(kFull, mask, 0);
+        b.fresh[k] = (mask >> lane) & 1u;
     }
-    __syncwarp();  // this row's sets are ordered before the next row's tests
+    __threadfence_block();
+    __syncwarp();
+    return true;
+}
+
+// Both phases back to back (the stand-alone bank kernel).
+template <int NPL>
+__device__ __forceinline__ void bloom_test_and_set(uint32_t *__restrict__ bits, uint32_t *s_sum,
+                                                   const BloomGeom &g,
+                                                   const uint32_t (&ids)[NPL], int cnt,
+                                                   bool (&fresh)[NPL]) {
+    BloomRow<NPL> b;
+    bloom_issue<NPL>(bits, s_sum, g, ids, cnt, b);
+    bloom_resolve<NPL>(bits, s_sum, g, ids, cnt, b);
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) fresh[k] = b.fresh[k];
 }
 
 // ------------------------------------------------------- distance table
@@ -347,71 +445,143 @@ __device__ __forceinline__ int first_unvisited(const uint8_t *s_vis, int from, i
 
 // ------------------------------------------------ worklist sort + merge
 // kernels.py:44-109 / engine.py:210-215 for one warp-owned worklist in smem.
-//   s_wl[0, cnt) sorted keys, s_vis flags; new keys key[c] (lane + 32c < F,
-//   unique, unsorted, SENTINEL elsewhere); s_sk scratch (>= F entries).
 // Keys in wl u new are unique (the Bloom filter has no false negatives), so
-// any correct merge is bit-identical to the reference's rank merge with its
-// a-first tie rule.  Sort = rank counting over warp shuffles; merge = each
-// element's final rank = own rank + rank in the other list (the paper's
-// Merge_LSet), written in place chunk by chunk from the
-// top so no unread entry is overwritten; entries ranked >= t are dropped.
-// Returns the new count min(t, cnt + F).
-template <int NPL>
-__device__ __forceinline__ int worklist_merge(uint64_t *s_wl, uint8_t *s_vis, int cnt, int t,
-                                              const uint64_t (&key)[NPL], int F,
-                                              uint64_t *s_sk) {
+// any correct sort/merge is bit-identical to the reference's rank merge with
+// its a-first tie rule.
+//
+// Only "survivors" reach the merge: when the worklist is full (cnt == t) a
+// new key >= wl[t-1] would land at rank >= t and be truncated by
+// merged[:, :t] (engine.py:213), so it is dropped before sorting.  The eager
+// winner is unaffected: a dropped key can only be the minimum when every
+// kept entry is visited, i.e. when the query converges this iteration.
+
+// s_sk[rank] = s_nk[j]: rank = #keys below it (n <= 128, broadcast reads)
+__device__ __forceinline__ void sort_keys(const uint64_t *s_nk, int n, uint64_t *s_sk) {
     const int lane = (int)lane_id();
-    int r1[NPL];
+    for (int j = lane; j < n; j += 32) {
+        const uint64_t k = s_nk[j];
+        int r = 0;
+        for (int i = 0; i < n; ++i) r += s_nk[i] < k;
+        s_sk[r] = k;
+    }
+    __syncwarp();
+}
+
+// Merge sorted survivors s_sk[0, n) into s_wl[0, cnt) (+ visited flags) and
+// truncate to t: each element's final rank = own rank + rank in the other
+// list (the paper's Merge_LSet).  Entries below the
+// first insertion point do not move; the rest are moved in place chunk by
+// chunk from the top so no unread entry is overwritten.  n <= 128.
+__device__ __forceinline__ int merge_sorted(uint64_t *s_wl, uint8_t *s_vis, int cnt, int t,
+                                            const uint64_t *s_sk, int n, int *first_out) {
+    const int lane = (int)lane_id();
+    if (n == 0) {
+        *first_out = cnt;
+        return cnt;
+    }
+    const int first = lower_bound_u64(s_wl, cnt, s_sk[0]);
+    *first_out = first;
+    int pos[4];
+    uint64_t kv[4];
 #pragma unroll
-    for (int c = 0; c < NPL; ++c) r1[c] = 0;
-#pragma unroll
-    for (int cs = 0; cs < NPL; ++cs) {
-        if (32 * cs < F) {
-            const int n = min(32, F - 32 * cs);
-            for (int i = 0; i < n; ++i) {
-                const uint64_t ki = __shfl_sync(kFull, key[cs], i);
-#pragma unroll
-                for (int c = 0; c < NPL; ++c) r1[c] += ki < key[c];
+    for (int c = 0; c < 4; ++c) {
+        const int j = lane + 32 * c;
+        pos[c] = t;
+        kv[c] = 0;
+        if (j < n) {
+            kv[c] = s_sk[j];
+            pos[c] = j + first + lower_bound_u64(s_wl + first, cnt - first, kv[c]);
+        }
+    }
+    __syncwarp();
+    if (first < cnt) {
+        for (int ch = (cnt - 1) >> 5; ch >= (first >> 5); --ch) {
+            const int i = ch * 32 + lane;
+            uint64_t v = 0;
+            uint8_t vv = 0;
+            int dst = t;
+            if (i >= first && i < cnt) {
+                v = s_wl[i];
+                vv = s_vis[i];
+                dst = i + lower_bound_u64(s_sk, n, v);
             }
+            __syncwarp();
+            if (dst < t) {
+                s_wl[dst] = v;
+                s_vis[dst] = vv;
+            }
+            __syncwarp();
         }
     }
-    int newpos[NPL];
 #pragma unroll
-    for (int c = 0; c < NPL; ++c) {
-        newpos[c] = t;  // dropped
-        if (lane + 32 * c < F) {
-            s_sk[r1[c]] = key[c];
-            newpos[c] = r1[c] + lower_bound_u64(s_wl, cnt, key[c]);
+    for (int c = 0; c < 4; ++c) {
+        if (pos[c] < t) {
+            s_wl[pos[c]] = kv[c];
+            s_vis[pos[c]] = 0;
         }
     }
     __syncwarp();
-    const int nch = (cnt + 31) >> 5;
-    for (int ch = nch - 1; ch >= 0; --ch) {
-        const int i = ch * 32 + lane;
-        uint64_t v = 0;
-        uint8_t vv = 0;
-        int dst = t;
-        if (i < cnt) {
-            v = s_wl[i];
-            vv = s_vis[i];
-            dst = i + lower_bound_u64(s_sk, F, v);
-        }
-        __syncwarp();
-        if (dst < t) {
-            s_wl[dst] = v;
-            s_vis[dst] = vv;
-        }
-        __syncwarp();
-    }
+    return min(t, cnt + n);
+}
+
+// ------------------------------------------------------- staged ADC ranges
+// acc += T[s][code_s] for s in [s0, s0 + 8) -- the same sequential f32 sum
+// as adc_codebook/adc_table, split into 8-subspace stages so that a
+// candidate whose partial sum already exceeds the worklist's last distance
+// can be dropped (f32 addition of non-negative terms is monotone, so
+// partial > thr implies final > thr: the survivor set is exact).
+template <int SUB>
+__device__ __forceinline__ float adc_cb_stage(float acc, const float *__restrict__ s_cb,
+                                              const float *__restrict__ s_q,
+                                              const int *__restrict__ s_off,
+                                              const int *__restrict__ s_sz, int s0, int ns,
+                                              uint64_t c8) {
+    if constexpr (SUB > 0) {
 #pragma unroll
-    for (int c = 0; c < NPL; ++c) {
-        if (newpos[c] < t) {
-            s_wl[newpos[c]] = key[c];
-            s_vis[newpos[c]] = 0;
+        for (int b = 0; b < 8; ++b) {
+            const int s = s0 + b;
+            const uint32_t c = (uint32_t)(c8 >> (8 * b)) & 0xFFu;
+            float e;
+            if constexpr (SUB == 4) {
+                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                                 *reinterpret_cast<const float4 *>(s_cb + (s * 256 + c) * 4));
+            } else if constexpr (SUB == 2) {
+                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                                 *reinterpret_cast<const float2 *>(s_cb + (s * 256 + c) * 2));
+            } else {
+                e = table_entry(s_q + s * SUB, s_cb + (s * 256 + c) * SUB, SUB);
+            }
+            acc = __fadd_rn(acc, e);
+        }
+    } else {
+        for (int b = 0; b < ns; ++b) {
+            const int s = s0 + b;
+            const int c = (int)((c8 >> (8 * b)) & 0xFFu);
+            const int off = s_off[s], sz = s_sz[s];
+            acc = __fadd_rn(acc, table_entry(s_q + off, s_cb + off * 256 + c * sz, sz));
         }
     }
-    __syncwarp();
-    return min(t, cnt + F);
+    return acc;
+}
+
+__device__ __forceinline__ float adc_tab_stage(float acc, const float *__restrict__ trow, int s0,
+                                               int ns, uint64_t c8) {
+    for (int b = 0; b < ns; ++b)
+        acc = __fadd_rn(acc, __ldg(trow + (s0 + b) * 256 + (int)((c8 >> (8 * b)) & 0xFFu)));
+    return acc;
+}
+
+// eight code bytes of a row starting at subspace s0 (fewer at the tail)
+template <bool ALIGNED8>
+__device__ __forceinline__ uint64_t load_code8(const uint8_t *__restrict__ row, int s0, int ns) {
+    if constexpr (ALIGNED8) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(row + s0));
+        return (uint64_t)v.x | ((uint64_t)v.y << 32);
+    } else {
+        uint64_t c8 = 0;
+        for (int b = 0; b < ns; ++b) c8 |= (uint64_t)__ldg(row + s0 + b) << (8 * b);
+        return c8;
+    }
 }
 
 }  // namespace bang

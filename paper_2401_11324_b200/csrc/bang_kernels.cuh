@@ -62,7 +62,8 @@ struct SearchParams {
     // shapes
     int32_t m, dim, R, medoid, k, t, vec_dtype, adc_variant, rerank, debug;
     int32_t smem_shared_bytes, per_warp_bytes;
-    int32_t off_q, off_wl, off_sk, off_fid, off_vis;  // byte offsets inside a warp region
+    int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum;  // warp region
+    int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -73,18 +74,6 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 
 __global__ void record_t0_kernel(unsigned long long *counters) {
     counters[kCtrT0] = globaltimer_ns();
-}
-
-// Score one candidate for the warp's query (ADC or exact distance).
-template <int SUB, int MV>
-__device__ __forceinline__ float score_node(const SearchParams &p, const float *s_cb,
-                                            const int *s_off, const int *s_sz,
-                                            const float *s_q, int64_t qid, uint32_t node) {
-    if (p.adc_variant == kAdcSmemCodebook)
-        return adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)node * p.m);
-    if (p.adc_variant == kAdcGlobalTable)
-        return adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)node * p.m);
-    return exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q);
 }
 
 // Top-k of unique keys keys[0, L) (global, written by this warp) into
@@ -115,17 +104,92 @@ __device__ __forceinline__ void warp_topk_write(const uint64_t *keys, int64_t L,
     }
 }
 
+// Staged ADC of the fresh neighbours s_fid[0, F) with survivor filtering
+// (keys < thr; thr = wl[t-1] when the worklist is full, else SENTINEL):
+// survivors' exact keys are compacted into s_nk; returns their count.
+template <int SUB, int MV>
+__device__ __forceinline__ int adc_survivors(const SearchParams &p, const float *s_cb,
+                                             const int *s_off, const int *s_sz,
+                                             const float *s_q, int64_t qid,
+                                             const uint32_t *s_fid, int F, float *s_acc,
+                                             uint8_t *s_alive, uint64_t thr, uint64_t *s_nk) {
+    const int lane = (int)lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    if (p.adc_variant == kAdcExact) {
+        int n = 0;
+        for (int base = 0; base < F; base += 32) {
+            const int a = base + lane;
+            uint64_t key = kSentinel;
+            if (a < F) {
+                const uint32_t node = s_fid[a];
+                key = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+            }
+            const bool keep = a < F && key < thr;
+            const unsigned bal = __ballot_sync(kFull, keep);
+            if (keep) s_nk[n + __popc(bal & lt)] = key;
+            n += __popc(bal);
+        }
+        __syncwarp();
+        return n;
+    }
+    const float thr_d = thr == kSentinel ? __int_as_float(0x7f800000) : key_dist(thr);
+    const float *trow = p.table + qid * (int64_t)p.m * 256;
+    const int m = p.m;
+    int n_alive = F;
+    for (int s0 = 0; s0 < m && n_alive > 0; s0 += 8) {
+        const int ns = min(8, m - s0);
+        const bool last = s0 + 8 >= m;
+        int n_keep = 0;
+        for (int base = 0; base < n_alive; base += 32) {
+            const int a = base + lane;
+            bool keep = false;
+            uint64_t key = 0;
+            int j = 0;
+            if (a < n_alive) {
+                j = s0 == 0 ? a : s_alive[a];
+                const uint32_t node = s_fid[j];
+                float acc = s0 == 0 ? 0.0f : s_acc[j];
+                const uint64_t c8 = load_code8<(MV > 0)>(p.codes + (int64_t)node * m, s0, ns);
+                if (p.adc_variant == kAdcSmemCodebook)
+                    acc = adc_cb_stage<SUB>(acc, s_cb, s_q, s_off, s_sz, s0, ns, c8);
+                else
+                    acc = adc_tab_stage(acc, trow, s0, ns, c8);
+                if (last) {
+                    key = pack_key(acc, node);
+                    keep = key < thr;
+                } else {
+                    keep = !(acc > thr_d);
+                    s_acc[j] = acc;
+                }
+            }
+            const unsigned bal = __ballot_sync(kFull, keep);
+            __syncwarp();  // this round's s_alive reads precede the compaction writes
+            if (keep) {
+                const int pos = n_keep + __popc(bal & lt);
+                if (last) s_nk[pos] = key;
+                else s_alive[pos] = (uint8_t)j;
+            }
+            n_keep += __popc(bal);
+        }
+        __syncwarp();
+        n_alive = n_keep;
+        if (last) return n_alive;
+    }
+    return 0;
+}
+
 // -------------------------------------------------------------------------
 // The fused persistent search kernel.  One warp owns one query at a time
 // (dynamic fetch from an atomic counter, so stragglers never idle an SM);
-// per-query state: worklist + visited flags + query vector in shared
-// memory, Bloom filter in HBM/L2, adjacency row of the next candidate in
-// registers.  Per iteration (engine.py:152-236):
-//   expand u -> Bloom test-and-set of u's neighbours (kernel 2) -> ADC of
-//   the fresh ones (kernel 3) -> eager winner = min(best fresh, first
-//   unvisited) and the winner's adjacency row is loaded NOW ("one hop
-//   ahead") -> sort + merge-truncate to t (kernel 4)
-//   -> converged when no unvisited entry is left.
+// per-query state: worklist + visited flags + query vector + Bloom summary
+// in shared memory, Bloom words in HBM/L2, the next candidate's adjacency
+// row in registers.  Per iteration (engine.py:152-236):
+//   expand u -> Bloom test-and-set of u's neighbours (kernel 2; atomics in
+//   flight) -> staged ADC of the fresh ones with survivor filtering
+//   (kernel 3) -> resolve the Bloom atomics -> sort survivors, eager winner
+//   = min(best survivor, first unvisited) and the winner's adjacency row is
+//   loaded NOW ("one hop ahead") -> merge + truncate to t
+//   (kernel 4) -> converged when the winner is gone or truncated.
 // At convergence the warp re-ranks its visit log with exact distances
 // (kernel 5) and writes the query's outputs.
 // -------------------------------------------------------------------------
@@ -158,8 +222,12 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
     float *s_q = reinterpret_cast<float *>(wbase + p.off_q);
     uint64_t *s_wl = reinterpret_cast<uint64_t *>(wbase + p.off_wl);
     uint64_t *s_sk = reinterpret_cast<uint64_t *>(wbase + p.off_sk);
+    uint64_t *s_nk = reinterpret_cast<uint64_t *>(wbase + p.off_nk);
     uint32_t *s_fid = reinterpret_cast<uint32_t *>(wbase + p.off_fid);
+    float *s_acc = reinterpret_cast<float *>(wbase + p.off_acc);
+    uint8_t *s_alive = wbase + p.off_alive;
     uint8_t *s_vis = wbase + p.off_vis;
+    uint32_t *s_sum = reinterpret_cast<uint32_t *>(wbase + p.off_sum);
     uint32_t *bits = p.bloom + (int64_t)slot * p.bloom_stride;
     uint64_t *rr = p.rr_scratch + (int64_t)slot * p.log_cap;
     const int t = p.t, R = p.R;
@@ -173,27 +241,38 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
         if (qi >= p.nq) break;
         const int64_t qid = p.query_map ? (int64_t)p.query_map[qi] : qi;
 
-        // query vector -> smem; clear this slot's filter; set the medoid
-        // (engine.py:127-128 set_all_rows)
+        // query vector -> smem; empty Bloom summary (the filter words are
+        // never cleared: unsummarised words read as 0); vis flags
         for (int j = lane; j < p.dim; j += 32) s_q[j] = __ldg(p.queries + qid * p.dim + j);
-        {
-            uint4 *b4 = reinterpret_cast<uint4 *>(bits);
-            const int64_t n4 = p.bloom_stride >> 2;
-            const uint4 z4 = make_uint4(0, 0, 0, 0);
-            for (int64_t i = lane; i < n4; i += 32) __stcg(b4 + i, z4);
-        }
+        for (int j = lane; j < p.sum_words; j += 32) s_sum[j] = 0u;
         for (int j = lane; j < t; j += 32) s_vis[j] = 0;
-        __threadfence_block();
         __syncwarp();
+        // medoid in the filter (engine.py:127-128 set_all_rows)
         if (lane == 0) {
-            atomicOr(bits + (p.medoid_p1 >> 5), 1u << (p.medoid_p1 & 31));
-            atomicOr(bits + (p.medoid_p2 >> 5), 1u << (p.medoid_p2 & 31));
+            const uint32_t w1 = p.medoid_p1 >> 5, w2 = p.medoid_p2 >> 5;
+            const uint32_t b1 = 1u << (p.medoid_p1 & 31), b2 = 1u << (p.medoid_p2 & 31);
+            if (w1 == w2) {
+                __stcg(bits + w1, b1 | b2);
+            } else {
+                __stcg(bits + w1, b1);
+                __stcg(bits + w2, b2);
+            }
+            s_sum[w1 >> 5] |= 1u << (w1 & 31);
+            s_sum[w2 >> 5] |= 1u << (w2 & 31);
         }
         // worklist = [key(score(medoid), medoid)] (engine.py:118-125)
         float d0 = 0.f;
-        if (lane == 0) d0 = score_node<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, (uint32_t)p.medoid);
-        d0 = __shfl_sync(kFull, d0, 0);
-        if (lane == 0) s_wl[0] = pack_key(d0, (uint32_t)p.medoid);
+        if (lane == 0) {
+            if (p.adc_variant == kAdcSmemCodebook)
+                d0 = adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)p.medoid * p.m);
+            else if (p.adc_variant == kAdcGlobalTable)
+                d0 = adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)p.medoid * p.m);
+            else
+                d0 = exact_sq_dist(p.vectors, p.vec_dtype, p.dim, p.medoid, s_q);
+            s_wl[0] = pack_key(d0, (uint32_t)p.medoid);
+        }
+        __threadfence_block();
+        __syncwarp();
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         uint32_t ids[NPL];
@@ -206,7 +285,6 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
         // log rows follow the pass order when a query map is given (retry pass)
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
-        __syncwarp();
 
         for (;;) {
             // ---- expand u (engine.py:163-178)
@@ -219,37 +297,33 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
             ++iters;
             st_probes += deg;
             // ---- kernel 2: Bloom test-and-set in adjacency order (engine.py:180-186)
-            bool fresh[NPL];
-            bloom_test_and_set<NPL>(bits, p.geom, ids, deg, fresh);
-            // ---- compact the fresh ids (warp-aggregated ballot + popc)
-            int F = 0;
+            BloomRow<NPL> br;
+            bloom_issue<NPL>(bits, s_sum, p.geom, ids, deg, br);
+            const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
+            int F = 0, n_s = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                // ---- compact the fresh ids (warp-aggregated ballot + popc)
+                F = 0;
 #pragma unroll
-            for (int k = 0; k < NPL; ++k) {
-                const unsigned b = __ballot_sync(kFull, fresh[k]);
-                if (fresh[k]) s_fid[F + __popc(b & ((1u << lane) - 1u))] = ids[k];
-                F += __popc(b);
+                for (int k = 0; k < NPL; ++k) {
+                    const unsigned b = __ballot_sync(kFull, br.fresh[k]);
+                    if (br.fresh[k]) s_fid[F + __popc(b & ((1u << lane) - 1u))] = ids[k];
+                    F += __popc(b);
+                }
+                __syncwarp();
+                // ---- kernel 3: staged ADC of the fresh neighbours (engine.py:188-199)
+                n_s = adc_survivors<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, s_fid, F, s_acc, s_alive, thr, s_nk);
+                // ---- the Bloom atomics' results (collision -> exact replay, redo)
+                if (pass == 0 && !bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br)) break;
             }
             st_fresh += F;
-            __syncwarp();
-            // ---- kernel 3: ADC of the fresh neighbours (engine.py:188-199)
-            uint64_t key[NPL];
-#pragma unroll
-            for (int c = 0; c < NPL; ++c) {
-                key[c] = kSentinel;
-                const int j = lane + 32 * c;
-                if (j < F) {
-                    const uint32_t node = s_fid[j];
-                    key[c] = pack_key(score_node<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, node), node);
-                }
-            }
-            // ---- eager winner (engine.py:201-205) and one-hop-ahead prefetch
-            uint64_t best = key[0];
-#pragma unroll
-            for (int c = 1; c < NPL; ++c) best = key[c] < best ? key[c] : best;
-            best = warp_min_u64(best);
+            // ---- sort survivors; eager winner (engine.py:201-205)
+            sort_keys(s_nk, n_s, s_sk);
             const int hpos = first_unvisited(s_vis, upos + 1, cnt);
             const uint64_t head = hpos < cnt ? s_wl[hpos] : kSentinel;
+            const uint64_t best = n_s > 0 ? s_sk[0] : kSentinel;
             const uint64_t winner = best < head ? best : head;
+            // ---- one-hop-ahead prefetch of the winner's adjacency row
             uint32_t nids[NPL];
             int ndeg = 0;
             if (winner != kSentinel) {
@@ -264,11 +338,20 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
 #pragma unroll
                 for (int k = 0; k < NPL; ++k) nids[k] = 0u;
             }
-            // ---- kernel 4: sort + merge + truncate (engine.py:210-215)
-            cnt = worklist_merge<NPL>(s_wl, s_vis, cnt, t, key, F, s_sk);
-            // ---- converge (engine.py:217-236)
-            upos = first_unvisited(s_vis, 0, cnt);
-            if (upos >= cnt) break;
+            // ---- kernel 4: merge + truncate (engine.py:210-215)
+            int first = 0;
+            const int old_cnt = cnt;
+            cnt = merge_sorted(s_wl, s_vis, cnt, t, s_sk, n_s, &first);
+            // ---- converge (engine.py:217-236): the winner is the new first
+            // unvisited entry unless it was truncated away
+            int wpos = t;
+            if (winner != kSentinel) {
+                if (best < head) wpos = first;
+                else wpos = hpos + lower_bound_u64(s_sk, n_s, head);
+            }
+            (void)old_cnt;
+            if (wpos >= t) break;
+            upos = wpos;
             if (p.debug && lane == 0 && s_wl[upos] != winner) atomicAdd(p.counters + kCtrDebugFail, 1ull);
             u = key_id(winner);
             deg = ndeg;
@@ -375,7 +458,7 @@ __global__ void bloom_bank_kernel(uint32_t *bits, int64_t count, int64_t words32
         const int cnt = (int)min((int64_t)32, hi - base);
         uint32_t id[1] = {lane < cnt ? ids[base + lane] : 0u};
         bool fr[1];
-        bloom_test_and_set<1>(b, g, id, cnt, fr);
+        bloom_test_and_set<1>(b, nullptr, g, id, cnt, fr);
         if (lane < cnt) fresh[base + lane] = fr[0] ? 1 : 0;
     }
 }
@@ -444,9 +527,10 @@ __global__ void merge_rows_kernel(const uint64_t *__restrict__ a, const uint8_t 
 // -------------------------------------------------------------------------
 // Kernel 4 (engine step) -- eager pick + sort + merge + truncate + converge
 // (engine.py:201-217) per worklist row, one warp per row, through the same
-// worklist_merge the fused kernel runs.
+// survivor filter / sort_keys / merge_sorted the fused kernel runs.
+// Shared memory per warp: wl keys (t), sorted + unsorted new keys (w each),
+// visited flags (t).
 // -------------------------------------------------------------------------
-template <int NPL>
 __global__ void worklist_update_kernel(uint64_t *wl_keys, uint8_t *wl_vis, int64_t rows, int t,
                                        const uint64_t *__restrict__ new_keys, int w,
                                        uint64_t *winner, uint8_t *done) {
@@ -454,11 +538,13 @@ __global__ void worklist_update_kernel(uint64_t *wl_keys, uint8_t *wl_vis, int64
     const int warp = threadIdx.x >> 5, lane = (int)lane_id();
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (row >= rows) return;
-    const int per_warp = ((t * 8 + 15) & ~15) + ((NPL * 32 * 8 + 15) & ~15) + ((t + 15) & ~15);
+    const int a_wl = (t * 8 + 15) & ~15, a_k = (w * 8 + 15) & ~15;
+    const int per_warp = a_wl + 2 * a_k + ((t + 15) & ~15);
     unsigned char *base = smem + (size_t)warp * per_warp;
     uint64_t *s_wl = reinterpret_cast<uint64_t *>(base);
-    uint64_t *s_sk = reinterpret_cast<uint64_t *>(base + ((t * 8 + 15) & ~15));
-    uint8_t *s_vis = base + ((t * 8 + 15) & ~15) + ((NPL * 32 * 8 + 15) & ~15);
+    uint64_t *s_sk = reinterpret_cast<uint64_t *>(base + a_wl);
+    uint64_t *s_nk = reinterpret_cast<uint64_t *>(base + a_wl + a_k);
+    uint8_t *s_vis = base + a_wl + 2 * a_k;
     uint64_t *gw = wl_keys + row * t;
     uint8_t *gv = wl_vis + row * t;
     int cnt = 0;
@@ -472,33 +558,28 @@ __global__ void worklist_update_kernel(uint64_t *wl_keys, uint8_t *wl_vis, int64
         }
         cnt += __popc(__ballot_sync(kFull, real));
     }
-    // new keys: compact the non-sentinel ones into lanes
-    uint64_t key[NPL];
-    int F = 0;
-#pragma unroll
-    for (int c = 0; c < NPL; ++c) key[c] = kSentinel;
+    __syncwarp();
+    // survivors: non-sentinel new keys that can rank below t
+    const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
+    int n = 0;
+    uint64_t best_all = kSentinel;
     for (int b = 0; b < w; b += 32) {
         const int i = b + lane;
         const uint64_t v = i < w ? new_keys[row * w + i] : kSentinel;
-        const unsigned m = __ballot_sync(kFull, v != kSentinel);
-        const int pos = F + __popc(m & ((1u << lane) - 1u));
-        // place v into (pos % 32, pos / 32) via smem staging
-        if (v != kSentinel) s_sk[pos] = v;
-        F += __popc(m);
+        best_all = v < best_all ? v : best_all;
+        const bool keep = v != kSentinel && v < thr;
+        const unsigned m = __ballot_sync(kFull, keep);
+        if (keep) s_nk[n + __popc(m & ((1u << lane) - 1u))] = v;
+        n += __popc(m);
     }
+    best_all = warp_min_u64(best_all);
     __syncwarp();
-#pragma unroll
-    for (int c = 0; c < NPL; ++c)
-        if (lane + 32 * c < F) key[c] = s_sk[lane + 32 * c];
-    __syncwarp();
-    uint64_t best = key[0];
-#pragma unroll
-    for (int c = 1; c < NPL; ++c) best = key[c] < best ? key[c] : best;
-    best = warp_min_u64(best);
+    sort_keys(s_nk, n, s_sk);
     const int hpos = first_unvisited(s_vis, 0, cnt);
     const uint64_t head = hpos < cnt ? s_wl[hpos] : kSentinel;
-    const uint64_t win = best < head ? best : head;
-    cnt = worklist_merge<NPL>(s_wl, s_vis, cnt, t, key, F, s_sk);
+    const uint64_t win = best_all < head ? best_all : head;  // engine.py:202-204 (all new keys)
+    int first = 0;
+    cnt = merge_sorted(s_wl, s_vis, cnt, t, s_sk, n, &first);
     const int upos = first_unvisited(s_vis, 0, cnt);
     for (int i = lane; i < t; i += 32) {
         gw[i] = i < cnt ? s_wl[i] : kSentinel;
