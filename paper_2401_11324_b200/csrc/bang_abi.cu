@@ -160,11 +160,13 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     pl.sum_words = (int)ceil_div(pl.bloom_stride, 32);
     pl.off_q = 0;
     pl.off_wl = (int)align_up((int64_t)ix->dim * 4, 16);
-    pl.off_sk = pl.off_wl + (int)align_up((int64_t)t * 8, 16);
-    pl.off_nk = pl.off_sk + (int)align_up((int64_t)rpad * 8, 16);
+    pl.off_nk = pl.off_wl + (int)align_up((int64_t)t * 8, 16);
     pl.off_fid = pl.off_nk + (int)align_up((int64_t)rpad * 8, 16);
     pl.off_acc = pl.off_fid + (int)align_up((int64_t)rpad * 4, 16);
     pl.off_alive = pl.off_acc + (int)align_up((int64_t)rpad * 4, 16);
+    // the sorted survivors (s_sk, rpad u64) reuse the fid+acc scratch: both
+    // are dead once the ADC has produced the survivor keys
+    pl.off_sk = pl.off_fid;
     pl.off_vis = pl.off_alive + (int)align_up(rpad, 16);
     pl.off_sum = pl.off_vis + (int)align_up(t, 16);
     pl.per_warp = pl.off_sum + (int)align_up((int64_t)pl.sum_words * 4, 16);
@@ -192,7 +194,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     }
     int64_t w = (ix->max_smem - pl.shared_bytes) / pl.per_warp;
     if (w < 1) return fail(BANG_E_PARAM, "t=%d needs %d B of shared memory per query", t, pl.per_warp);
-    pl.warps = (int)std::min<int64_t>(32, w);
+    pl.warps = (int)std::min<int64_t>(kMaxSearchThreads / 32, w);
     pl.smem = pl.shared_bytes + pl.warps * pl.per_warp;
     const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);
     if (!kfn) return fail(BANG_E_STATE, "no kernel instance for npl=%d sub=%d mv=%d", pl.npl, pl.sub, pl.mv);

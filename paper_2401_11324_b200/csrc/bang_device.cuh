@@ -585,3 +585,38 @@ __device__ __forceinline__ uint64_t load_code8(const uint8_t *__restrict__ row, 
 }
 
 }  // namespace bang
+
+namespace bang {
+// 16-subspace stages for rows of m = 16*MV codes read as uint4 vectors.
+template <int SUB>
+__device__ __forceinline__ float adc_cb_stage16(float acc, const float *__restrict__ s_cb,
+                                                const float *__restrict__ s_q, int s0, uint4 cv) {
+    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+    for (int b = 0; b < 16; ++b) {
+        const int s = s0 + b;
+        const uint32_t c = (w[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
+        float e;
+        if constexpr (SUB == 4) {
+            e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                             *reinterpret_cast<const float4 *>(s_cb + (s * 256 + c) * 4));
+        } else if constexpr (SUB == 2) {
+            e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                             *reinterpret_cast<const float2 *>(s_cb + (s * 256 + c) * 2));
+        } else {
+            e = table_entry(s_q + s * SUB, s_cb + (s * 256 + c) * SUB, SUB);
+        }
+        acc = __fadd_rn(acc, e);
+    }
+    return acc;
+}
+
+__device__ __forceinline__ float adc_tab_stage16(float acc, const float *__restrict__ trow, int s0,
+                                                 uint4 cv) {
+    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+    for (int b = 0; b < 16; ++b)
+        acc = __fadd_rn(acc, __ldg(trow + (s0 + b) * 256 + ((w[b >> 2] >> ((b & 3) * 8)) & 0xFFu)));
+    return acc;
+}
+}  // namespace bang

@@ -29,6 +29,10 @@ enum Counter {
     kCtrCount = 8,
 };
 
+// 24 warps x 32 lanes: leaves ptxas 80 registers per thread; shared memory
+// already caps the CTA near 24 warps at d = 128.
+constexpr int kMaxSearchThreads = 768;
+
 struct SearchParams {
     // index (HBM, or host-mapped for the graph/vectors)
     const uint8_t *codes;
@@ -178,6 +182,93 @@ __device__ __forceinline__ int adc_survivors(const SearchParams &p, const float 
     return 0;
 }
 
+// 16-byte-code fast path of kernel 3 (m = 16*MV, 16-subspace stages).
+// Stage A runs in the lane that owns each probe (codes c0 prefetched with
+// the Bloom words); survivors (partial sum <= thr) are compacted into
+// s_fid/s_acc and the remaining stages load the next 16 code bytes of the
+// survivors only.  Survivor keys (< thr) end up compacted in s_nk.
+template <int NPL, int SUB, int MV>
+__device__ __forceinline__ int adc_fast_path(const SearchParams &p, const float *s_cb,
+                                             const float *s_q, int64_t qid,
+                                             const uint32_t (&ids)[NPL], const bool (&fresh)[NPL],
+                                             const uint4 (&c0)[NPL], uint64_t thr, uint32_t *s_fid,
+                                             float *s_acc, uint64_t *s_nk, int *F_out) {
+    const int lane = (int)lane_id();
+    const unsigned lt = (1u << lane) - 1u;
+    const float thr_d = thr == kSentinel ? __int_as_float(0x7f800000) : key_dist(thr);
+    const float *trow = p.table + qid * (int64_t)p.m * 256;
+    const bool cb = p.adc_variant == kAdcSmemCodebook;
+    int F = 0, n_alive = 0;
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) {
+        bool keep = false;
+        float acc = 0.0f;
+        uint64_t key = 0;
+        if (fresh[k]) {
+            acc = cb ? adc_cb_stage16<SUB>(0.0f, s_cb, s_q, 0, c0[k]) : adc_tab_stage16(0.0f, trow, 0, c0[k]);
+            if (MV == 1) {
+                key = pack_key(acc, ids[k]);
+                keep = key < thr;
+            } else {
+                keep = !(acc > thr_d);
+            }
+        }
+        F += __popc(__ballot_sync(kFull, fresh[k]));
+        const unsigned bal = __ballot_sync(kFull, keep);
+        if (keep) {
+            const int pos = n_alive + __popc(bal & lt);
+            if (MV == 1) {
+                s_nk[pos] = key;
+            } else {
+                s_fid[pos] = ids[k];
+                s_acc[pos] = acc;
+            }
+        }
+        n_alive += __popc(bal);
+    }
+    *F_out = F;
+    __syncwarp();
+#pragma unroll
+    for (int st = 1; st < MV; ++st) {
+        const bool last = st == MV - 1;
+        int n_keep = 0;
+        for (int base = 0; base < n_alive; base += 32) {
+            const int a = base + lane;
+            bool keep = false;
+            uint64_t key = 0;
+            uint32_t node = 0;
+            float acc = 0.0f;
+            if (a < n_alive) {
+                node = s_fid[a];
+                acc = s_acc[a];
+                const uint4 cv = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)node * p.m) + st);
+                acc = cb ? adc_cb_stage16<SUB>(acc, s_cb, s_q, 16 * st, cv) : adc_tab_stage16(acc, trow, 16 * st, cv);
+                if (last) {
+                    key = pack_key(acc, node);
+                    keep = key < thr;
+                } else {
+                    keep = !(acc > thr_d);
+                }
+            }
+            const unsigned bal = __ballot_sync(kFull, keep);
+            __syncwarp();  // this round's reads precede the compaction writes
+            if (keep) {
+                const int pos = n_keep + __popc(bal & lt);
+                if (last) {
+                    s_nk[pos] = key;
+                } else {
+                    s_fid[pos] = node;
+                    s_acc[pos] = acc;
+                }
+            }
+            n_keep += __popc(bal);
+        }
+        __syncwarp();
+        n_alive = n_keep;
+    }
+    return n_alive;
+}
+
 // -------------------------------------------------------------------------
 // The fused persistent search kernel.  One warp owns one query at a time
 // (dynamic fetch from an atomic counter, so stragglers never idle an SM);
@@ -194,7 +285,7 @@ __device__ __forceinline__ int adc_survivors(const SearchParams &p, const float 
 // (kernel 5) and writes the query's outputs.
 // -------------------------------------------------------------------------
 template <int NPL, int SUB, int MV>
-__global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
+__global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const SearchParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = (int)lane_id();
     const int warp = threadIdx.x >> 5;
@@ -297,24 +388,46 @@ __global__ void __launch_bounds__(1024, 1) search_kernel(const SearchParams p) {
             ++iters;
             st_probes += deg;
             // ---- kernel 2: Bloom test-and-set in adjacency order (engine.py:180-186)
+            // (16-byte code path: the first 16 code bytes of every neighbour are
+            // requested together with the Bloom words, off the critical path)
+            uint4 c0[NPL];
+            if constexpr (MV > 0) {
+#pragma unroll
+                for (int k = 0; k < NPL; ++k)
+                    if (lane + 32 * k < deg)
+                        c0[k] = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)ids[k] * p.m));
+            }
             BloomRow<NPL> br;
             bloom_issue<NPL>(bits, s_sum, p.geom, ids, deg, br);
             const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
             int F = 0, n_s = 0;
-            for (int pass = 0; pass < 2; ++pass) {
-                // ---- compact the fresh ids (warp-aggregated ballot + popc)
-                F = 0;
-#pragma unroll
-                for (int k = 0; k < NPL; ++k) {
-                    const unsigned b = __ballot_sync(kFull, br.fresh[k]);
-                    if (br.fresh[k]) s_fid[F + __popc(b & ((1u << lane) - 1u))] = ids[k];
-                    F += __popc(b);
+            if constexpr (MV > 0) {
+                // ---- kernel 3: staged ADC; stage A (subspaces 0-15) in the
+                // probe's own lane, later stages on compacted survivors
+                if (p.adc_variant != kAdcExact) {
+                    n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid, s_acc,
+                                                      s_nk, &F);
+                    if (bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br))
+                        n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid,
+                                                          s_acc, s_nk, &F);
                 }
-                __syncwarp();
-                // ---- kernel 3: staged ADC of the fresh neighbours (engine.py:188-199)
-                n_s = adc_survivors<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, s_fid, F, s_acc, s_alive, thr, s_nk);
-                // ---- the Bloom atomics' results (collision -> exact replay, redo)
-                if (pass == 0 && !bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br)) break;
+            } else {
+                for (int pass = 0; pass < 2; ++pass) {
+                    // ---- compact the fresh ids (warp-aggregated ballot + popc)
+                    F = 0;
+#pragma unroll
+                    for (int k = 0; k < NPL; ++k) {
+                        const unsigned b = __ballot_sync(kFull, br.fresh[k]);
+                        if (br.fresh[k]) s_fid[F + __popc(b & ((1u << lane) - 1u))] = ids[k];
+                        F += __popc(b);
+                    }
+                    __syncwarp();
+                    // ---- kernel 3: staged ADC of the fresh neighbours (engine.py:188-199)
+                    n_s = adc_survivors<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, s_fid, F, s_acc, s_alive, thr,
+                                                 s_nk);
+                    // ---- the Bloom atomics' results (collision -> exact replay, redo)
+                    if (pass == 0 && !bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br)) break;
+                }
             }
             st_fresh += F;
             // ---- sort survivors; eager winner (engine.py:201-205)
