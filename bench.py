@@ -138,7 +138,7 @@ def main():
     ap.add_argument("--cache", default=os.environ.get("BANG_BENCH_CACHE", "/tmp/bang_bench_cache"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
-    ap.add_argument("--variant", default="auto", choices=("auto", "smem", "table"))
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "codebook", "hbm-table"))
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -171,6 +171,7 @@ def main():
     searcher = GraphSearcher(k=k, t=max(T_SWEEP), mode="in_memory", bloom_entries=args.bloom,
                              batch_size=nq)
     searcher.fit(art["base"], graph=art["graph"], codebook=art["codebook"], codes=art["codes"])
+    searcher.set_adc_variant(args.variant)
 
     # ---- worklist size at recall >= target (the metric's operating point)
     sweep = []
@@ -223,7 +224,8 @@ def main():
         return
 
     # ---- device-resident timing (value)
-    flags = _lib.RERANK | ({"auto": 0, "smem": _lib.TABLE_SMEM, "table": _lib.TABLE_GLOBAL}[args.variant])
+    flags = _lib.RERANK | {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
+                           "hbm-table": _lib.TABLE_GLOBAL}[args.variant]
     dev = torch.device("cuda", local)
     dq = torch.from_numpy(np.ascontiguousarray(shard["queries"], np.float32)).to(dev)
     d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)

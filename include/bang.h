@@ -48,8 +48,11 @@ typedef int32_t bang_status;
 #define BANG_RERANK 1          /* GraphSearcher(rerank=True), engine.py:254-262  */
 #define BANG_DEBUG_CHECKS 2    /* GraphSearcher(debug_checks=True), engine.py:169-227 */
 #define BANG_EXACT_DISTANCE 4  /* mode="exact_distance", engine.py:120-124,188-193 */
-#define BANG_TABLE_GLOBAL 8    /* force the HBM distance-table variant of ADC    */
-#define BANG_TABLE_SMEM 16     /* force the smem-codebook variant (error if it does not fit) */
+#define BANG_TABLE_GLOBAL 8    /* ADC from a distance table in HBM (kernel 1 first)   */
+#define BANG_TABLE_SMEM 16     /* ADC from a per-query table in shared memory         */
+#define BANG_CODEBOOK_SMEM 32  /* ADC recomputing entries from a CTA-shared codebook  */
+/* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
+ *  the shared codebook, else the HBM table)                                */
 
 typedef struct bang_index bang_index;
 
@@ -63,7 +66,7 @@ typedef struct bang_search_stats {
     int32_t slots;            /* concurrent query slots (warps) of the kernel   */
     int32_t warps_per_cta;
     int32_t ctas;
-    int32_t adc_variant;      /* 0 = smem codebook, 1 = HBM table, 2 = exact    */
+    int32_t adc_variant;      /* 0 smem codebook, 1 HBM table, 2 exact, 3 smem table */
     float kernel_ms;          /* device time of the fused search kernel(s)      */
     float table_ms;           /* device time of the PQ-table kernel (0 if none)  */
     int64_t algorithmic_bytes;/* HBM bytes the search must move     */

@@ -30,6 +30,8 @@ DEBUG_CHECKS = 2
 EXACT_DISTANCE = 4
 TABLE_GLOBAL = 8
 TABLE_SMEM = 16
+CODEBOOK_SMEM = 32
+ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -124,7 +124,7 @@ struct Plan {
     int npl = 2, sub = 0, mv = 0;
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
-    int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum;
+    int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;
     int sum_words = 0;
     int64_t bloom_stride = 0;
 };
@@ -171,20 +171,35 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     pl.off_sum = pl.off_vis + (int)align_up(t, 16);
     pl.per_warp = pl.off_sum + (int)align_up((int64_t)pl.sum_words * 4, 16);
     const int mv = (ix->m % 16 == 0 && ix->m / 16 >= 2 && ix->m / 16 <= 3) ? ix->m / 16 : 0;
+    const int64_t tab_bytes = (int64_t)ix->m * 256 * 4;
+    const int64_t cb_shared = align_up(cb_bytes + 8LL * ix->m, 16);
     if (exact) {
         pl.variant = kAdcExact;
     } else if (flags & BANG_TABLE_GLOBAL) {
         pl.variant = kAdcGlobalTable;
-    } else {
-        const int64_t shared = align_up(cb_bytes + 8LL * ix->m, 16);
-        const int64_t w = (ix->max_smem - shared) / pl.per_warp;
-        if (w >= 8 || ((flags & BANG_TABLE_SMEM) && w >= 1)) pl.variant = kAdcSmemCodebook;
-        else if (flags & BANG_TABLE_SMEM)
+    } else if (flags & BANG_CODEBOOK_SMEM) {
+        if ((ix->max_smem - cb_shared) / pl.per_warp < 1)
             return fail(BANG_E_PARAM, "smem codebook (%lld B) does not fit", (long long)cb_bytes);
-        else pl.variant = kAdcGlobalTable;
+        pl.variant = kAdcSmemCodebook;
+    } else if (flags & BANG_TABLE_SMEM) {
+        if (ix->max_smem / (pl.per_warp + tab_bytes) < 1)
+            return fail(BANG_E_PARAM, "a %lld B per-query table does not fit in shared memory", (long long)tab_bytes);
+        pl.variant = kAdcSmemTable;
+    } else if (ix->max_smem / (pl.per_warp + tab_bytes) >= 4) {
+        pl.variant = kAdcSmemTable;   // the paper's layout: per-query table in smem
+    } else if ((ix->max_smem - cb_shared) / pl.per_warp >= 8) {
+        pl.variant = kAdcSmemCodebook;
+    } else {
+        pl.variant = kAdcGlobalTable;
     }
+    pl.off_tab = pl.per_warp;
+    if (pl.variant == kAdcSmemTable) pl.per_warp += (int)tab_bytes;
     if (pl.variant == kAdcSmemCodebook) {
-        pl.shared_bytes = (int)align_up(cb_bytes + 8LL * ix->m, 16);
+        pl.shared_bytes = (int)cb_shared;
+        pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
+        pl.mv = pl.sub ? mv : 0;
+    } else if (pl.variant == kAdcSmemTable) {
+        pl.shared_bytes = 0;
         pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
         pl.mv = pl.sub ? mv : 0;
     } else {
@@ -273,6 +288,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_vis = pl.off_vis;
     p.off_sum = pl.off_sum;
     p.sum_words = pl.sum_words;
+    p.off_tab = pl.off_tab;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);

@@ -24,7 +24,10 @@ constexpr uint64_t kFnvOffsetH2 = (kFnvOffset ^ 0x5Aull) * kFnvPrime;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 enum VecDtype { kVecF32 = 0, kVecU8 = 1, kVecI8 = 2 };
-enum AdcVariant { kAdcSmemCodebook = 0, kAdcGlobalTable = 1, kAdcExact = 2 };
+// 0: CTA-shared codebook, entries recomputed per lookup; 1: HBM table built by
+// kernel 1; 2: exact distances (exact_distance mode); 3: per-query table in
+// the warp's shared memory, built at query start (the paper's layout).
+enum AdcVariant { kAdcSmemCodebook = 0, kAdcGlobalTable = 1, kAdcExact = 2, kAdcSmemTable = 3 };
 
 // kernels.py:25-29 -- non-negative f32 bit patterns are monotone, so the
 // u64 order is the (dist, id) lexicographic order.
@@ -284,6 +287,37 @@ __device__ __forceinline__ float table_entry4(float4 q, float4 c) {
     return __fadd_rn(acc, __fmul_rn(d3, d3));
 }
 
+// Per-query table in shared memory (variant D): entries of pq.py:290-294 for
+// all (s, c), written by the warp's lanes; centroids read from global/L2.
+template <int SUB>
+__device__ __forceinline__ void build_table_warp(float *s_tab, const float *__restrict__ s_q,
+                                                 const float *__restrict__ centroids,
+                                                 const int32_t *__restrict__ sub_off,
+                                                 const int32_t *__restrict__ sub_size, int m) {
+    for (int idx = (int)lane_id(); idx < m * 256; idx += 32) {
+        const int s = idx >> 8, c = idx & 255;
+        float e;
+        if constexpr (SUB == 4) {
+            e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                             __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
+        } else if constexpr (SUB == 2) {
+            e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                             __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
+        } else {
+            const int off = __ldg(sub_off + s), sz = __ldg(sub_size + s);
+            const float *src = centroids + (int64_t)off * 256 + c * sz;
+            float dd = __fsub_rn(s_q[off], __ldg(src));
+            float acc = __fmul_rn(dd, dd);
+            for (int j = 1; j < sz; ++j) {
+                dd = __fsub_rn(s_q[off + j], __ldg(src + j));
+                acc = __fadd_rn(acc, __fmul_rn(dd, dd));
+            }
+            e = acc;
+        }
+        s_tab[idx] = e;
+    }
+}
+
 // ------------------------------------------------------------------ ADC
 // engine.py:99-105: acc = 0f; acc += T[s][code[s]] for s = 0..m-1 (f32).
 // Variant A (smem codebook): T[s][c] is recomputed from the CTA-resident
@@ -332,9 +366,10 @@ __device__ __forceinline__ float adc_codebook(const float *__restrict__ s_cb,
     return acc;
 }
 
-// Variant B (HBM table from kernel 1): the reference's literal data flow.
+// Variants B/D (table from kernel 1 in HBM, or the warp's smem table): the
+// reference's literal data flow.  Plain loads: trow may point to either.
 template <int MV>
-__device__ __forceinline__ float adc_table(const float *__restrict__ trow, int m,
+__device__ __forceinline__ float adc_table(const float *trow, int m,
                                            const uint8_t *__restrict__ code_row) {
     float acc = 0.0f;
     if constexpr (MV > 0) {
@@ -348,11 +383,11 @@ __device__ __forceinline__ float adc_table(const float *__restrict__ trow, int m
             for (int b = 0; b < 16; ++b) {
                 const int s = v * 16 + b;
                 const uint32_t c = (w[b >> 2] >> ((b & 3) * 8)) & 0xFFu;
-                acc = __fadd_rn(acc, __ldg(trow + s * 256 + c));
+                acc = __fadd_rn(acc, trow[s * 256 + c]);
             }
         }
     } else {
-        for (int s = 0; s < m; ++s) acc = __fadd_rn(acc, __ldg(trow + s * 256 + __ldg(code_row + s)));
+        for (int s = 0; s < m; ++s) acc = __fadd_rn(acc, trow[s * 256 + __ldg(code_row + s)]);
     }
     return acc;
 }
@@ -564,10 +599,10 @@ __device__ __forceinline__ float adc_cb_stage(float acc, const float *__restrict
     return acc;
 }
 
-__device__ __forceinline__ float adc_tab_stage(float acc, const float *__restrict__ trow, int s0,
+__device__ __forceinline__ float adc_tab_stage(float acc, const float *trow, int s0,
                                                int ns, uint64_t c8) {
     for (int b = 0; b < ns; ++b)
-        acc = __fadd_rn(acc, __ldg(trow + (s0 + b) * 256 + (int)((c8 >> (8 * b)) & 0xFFu)));
+        acc = __fadd_rn(acc, trow[(s0 + b) * 256 + (int)((c8 >> (8 * b)) & 0xFFu)]);
     return acc;
 }
 
@@ -611,12 +646,12 @@ __device__ __forceinline__ float adc_cb_stage16(float acc, const float *__restri
     return acc;
 }
 
-__device__ __forceinline__ float adc_tab_stage16(float acc, const float *__restrict__ trow, int s0,
+__device__ __forceinline__ float adc_tab_stage16(float acc, const float *trow, int s0,
                                                  uint4 cv) {
     const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
     for (int b = 0; b < 16; ++b)
-        acc = __fadd_rn(acc, __ldg(trow + (s0 + b) * 256 + ((w[b >> 2] >> ((b & 3) * 8)) & 0xFFu)));
+        acc = __fadd_rn(acc, trow[(s0 + b) * 256 + ((w[b >> 2] >> ((b & 3) * 8)) & 0xFFu)]);
     return acc;
 }
 }  // namespace bang

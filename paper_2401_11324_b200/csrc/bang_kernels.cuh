@@ -66,7 +66,7 @@ struct SearchParams {
     // shapes
     int32_t m, dim, R, medoid, k, t, vec_dtype, adc_variant, rerank, debug;
     int32_t smem_shared_bytes, per_warp_bytes;
-    int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum;  // warp region
+    int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
 };
 
@@ -116,7 +116,8 @@ __device__ __forceinline__ int adc_survivors(const SearchParams &p, const float 
                                              const int *s_off, const int *s_sz,
                                              const float *s_q, int64_t qid,
                                              const uint32_t *s_fid, int F, float *s_acc,
-                                             uint8_t *s_alive, uint64_t thr, uint64_t *s_nk) {
+                                             uint8_t *s_alive, uint64_t thr, uint64_t *s_nk,
+                                             const float *s_tab) {
     const int lane = (int)lane_id();
     const unsigned lt = (1u << lane) - 1u;
     if (p.adc_variant == kAdcExact) {
@@ -137,7 +138,7 @@ __device__ __forceinline__ int adc_survivors(const SearchParams &p, const float 
         return n;
     }
     const float thr_d = thr == kSentinel ? __int_as_float(0x7f800000) : key_dist(thr);
-    const float *trow = p.table + qid * (int64_t)p.m * 256;
+    const float *trow = p.adc_variant == kAdcSmemTable ? s_tab : p.table + qid * (int64_t)p.m * 256;
     const int m = p.m;
     int n_alive = F;
     for (int s0 = 0; s0 < m && n_alive > 0; s0 += 8) {
@@ -192,11 +193,12 @@ __device__ __forceinline__ int adc_fast_path(const SearchParams &p, const float 
                                              const float *s_q, int64_t qid,
                                              const uint32_t (&ids)[NPL], const bool (&fresh)[NPL],
                                              const uint4 (&c0)[NPL], uint64_t thr, uint32_t *s_fid,
-                                             float *s_acc, uint64_t *s_nk, int *F_out) {
+                                             float *s_acc, uint64_t *s_nk, const float *s_tab,
+                                             int *F_out) {
     const int lane = (int)lane_id();
     const unsigned lt = (1u << lane) - 1u;
     const float thr_d = thr == kSentinel ? __int_as_float(0x7f800000) : key_dist(thr);
-    const float *trow = p.table + qid * (int64_t)p.m * 256;
+    const float *trow = p.adc_variant == kAdcSmemTable ? s_tab : p.table + qid * (int64_t)p.m * 256;
     const bool cb = p.adc_variant == kAdcSmemCodebook;
     int F = 0, n_alive = 0;
 #pragma unroll
@@ -319,6 +321,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
     uint8_t *s_alive = wbase + p.off_alive;
     uint8_t *s_vis = wbase + p.off_vis;
     uint32_t *s_sum = reinterpret_cast<uint32_t *>(wbase + p.off_sum);
+    float *s_tab = reinterpret_cast<float *>(wbase + p.off_tab);
     uint32_t *bits = p.bloom + (int64_t)slot * p.bloom_stride;
     uint64_t *rr = p.rr_scratch + (int64_t)slot * p.log_cap;
     const int t = p.t, R = p.R;
@@ -338,6 +341,10 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
         for (int j = lane; j < p.sum_words; j += 32) s_sum[j] = 0u;
         for (int j = lane; j < t; j += 32) s_vis[j] = 0;
         __syncwarp();
+        if (p.adc_variant == kAdcSmemTable) {  // kernel 1 for this query, into smem
+            build_table_warp<SUB>(s_tab, s_q, p.centroids, p.sub_off, p.sub_size, p.m);
+            __syncwarp();
+        }
         // medoid in the filter (engine.py:127-128 set_all_rows)
         if (lane == 0) {
             const uint32_t w1 = p.medoid_p1 >> 5, w2 = p.medoid_p2 >> 5;
@@ -358,6 +365,8 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                 d0 = adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)p.medoid * p.m);
             else if (p.adc_variant == kAdcGlobalTable)
                 d0 = adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)p.medoid * p.m);
+            else if (p.adc_variant == kAdcSmemTable)
+                d0 = adc_table<MV>(s_tab, p.m, p.codes + (int64_t)p.medoid * p.m);
             else
                 d0 = exact_sq_dist(p.vectors, p.vec_dtype, p.dim, p.medoid, s_q);
             s_wl[0] = pack_key(d0, (uint32_t)p.medoid);
@@ -406,10 +415,10 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                 // probe's own lane, later stages on compacted survivors
                 if (p.adc_variant != kAdcExact) {
                     n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid, s_acc,
-                                                      s_nk, &F);
+                                                      s_nk, s_tab, &F);
                     if (bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br))
                         n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid,
-                                                          s_acc, s_nk, &F);
+                                                          s_acc, s_nk, s_tab, &F);
                 }
             } else {
                 for (int pass = 0; pass < 2; ++pass) {
@@ -424,7 +433,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                     __syncwarp();
                     // ---- kernel 3: staged ADC of the fresh neighbours (engine.py:188-199)
                     n_s = adc_survivors<SUB, MV>(p, s_cb, s_off, s_sz, s_q, qid, s_fid, F, s_acc, s_alive, thr,
-                                                 s_nk);
+                                                 s_nk, s_tab);
                     // ---- the Bloom atomics' results (collision -> exact replay, redo)
                     if (pass == 0 && !bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br)) break;
                 }

@@ -278,8 +278,21 @@ class GraphSearcher(BaseEstimator):
         self.engine_vectors_ = base if self.mode != "pipelined" else None
         return self
 
+    _ADC_FLAGS = {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
+                  "hbm-table": _lib.TABLE_GLOBAL}
+
+    def set_adc_variant(self, name: str) -> "GraphSearcher":
+        """Pick the ADC data flow (results are identical for all of them):
+        "auto", "smem-table" (per-query table in shared memory, the paper's
+        layout), "codebook" (entries recomputed from a CTA-shared codebook) or
+        "hbm-table" (kernel 1 writes the table to HBM)."""
+        if name not in self._ADC_FLAGS:
+            raise ParameterError(f"unknown ADC variant {name!r}")
+        self._adc_variant = name
+        return self
+
     def _flags(self) -> int:
-        flags = 0
+        flags = self._ADC_FLAGS[getattr(self, "_adc_variant", "auto")]
         if self.rerank:
             flags |= _lib.RERANK
         if self.debug_checks:

@@ -214,17 +214,16 @@ def test_pipelined_equals_in_memory_and_reference(name):
     _assert_same(res, g["ids"], g["dists"], g["iterations"], gu.logs(g["log_offsets"], g["log_ids"]))
 
 
-@pytest.mark.parametrize("name", ["search_vamana_f32.npz", "search_vamana_r40_uneven.npz",
-                                  "search_random_r64.npz", "search_vamana_bloom61.npz"])
-def test_global_table_variant_matches(name):
-    """The HBM-table ADC variant (kernel 1 -> table -> kernel 3 path)."""
-    from paper_2401_11324_b200 import _lib
+@pytest.mark.parametrize("variant,code", [("hbm-table", 1), ("codebook", 0), ("smem-table", 3)])
+@pytest.mark.parametrize("name", ["search_toy_k2.npz", "search_vamana_f32.npz", "search_vamana_r40_uneven.npz",
+                                  "search_random_r64.npz", "search_vamana_bloom61.npz", "search_vamana_u8.npz"])
+def test_every_adc_variant_matches(name, variant, code):
+    """All ADC data flows (HBM table from kernel 1, shared codebook, per-query
+    smem table) give the reference's results bit for bit."""
     g = gu.load(name)
-    s = _searcher_from_golden(g)
-    orig = s._flags
-    s._flags = lambda: orig() | _lib.TABLE_GLOBAL
+    s = _searcher_from_golden(g).set_adc_variant(variant)
     res = s.search(g["queries"])
-    assert s.last_stats()["adc_variant"] == 1
+    assert s.last_stats()["adc_variant"] == code
     _assert_same(res, g["ids"], g["dists"], g["iterations"], gu.logs(g["log_offsets"], g["log_ids"]))
 
 
@@ -300,11 +299,12 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
-    res = s.search(q)
     want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
                     adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
                     k=10, t=t, bloom_entries=399_887, threads=8)
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    for variant in ("auto", "smem-table", "codebook", "hbm-table"):
+        res = s.set_adc_variant(variant).search(q)
+        _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
 def test_visit_log_overflow_retry_is_exact():
