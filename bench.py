@@ -138,6 +138,7 @@ def main():
     ap.add_argument("--cache", default=os.environ.get("BANG_BENCH_CACHE", "/tmp/bang_bench_cache"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
+    ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
     ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "codebook", "hbm-table"))
     args = ap.parse_args()
 
@@ -226,6 +227,8 @@ def main():
     # ---- device-resident timing (value)
     flags = _lib.RERANK | {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
                            "hbm-table": _lib.TABLE_GLOBAL}[args.variant]
+    if args.phases:
+        flags |= _lib.PROFILE_PHASES
     dev = torch.device("cuda", local)
     dq = torch.from_numpy(np.ascontiguousarray(shard["queries"], np.float32)).to(dev)
     d_ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
@@ -346,6 +349,11 @@ def main():
            "search_stats": {kk: s_last[kk] for kk in ("iterations", "probes", "fresh", "rerank_cands", "slots",
                                                       "warps_per_cta", "ctas", "adc_variant", "retries")},
            "step_ms": [round(x, 4) for x in step_ms]}
+    if args.phases:
+        pc = s_last["phase_cycles"]
+        it = max(1, s_last["iterations"])
+        names = ["adj_wait", "expand", "bloom_issue", "adc", "bloom_resolve", "sort_eager_prefetch", "merge"]
+        out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -51,6 +51,7 @@ typedef int32_t bang_status;
 #define BANG_TABLE_GLOBAL 8    /* ADC from a distance table in HBM (kernel 1 first)   */
 #define BANG_TABLE_SMEM 16     /* ADC from a per-query table in shared memory         */
 #define BANG_CODEBOOK_SMEM 32  /* ADC recomputing entries from a CTA-shared codebook  */
+#define BANG_PROFILE_PHASES 64 /* accumulate per-phase cycles (diagnostics, slower)  */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 
@@ -71,6 +72,10 @@ typedef struct bang_search_stats {
     float table_ms;           /* device time of the PQ-table kernel (0 if none)  */
     int64_t algorithmic_bytes;/* HBM bytes the search must move     */
     int64_t adc_bytes;        /* fresh * (m + 12)               */
+    int64_t phase_cycles[8];  /* BANG_PROFILE_PHASES: SM cycles per iteration phase,
+                                 summed over warps: 0 adjacency wait, 1 expand,
+                                 2 Bloom issue, 3 ADC, 4 Bloom resolve, 5 sort +
+                                 eager + prefetch, 6 merge + converge, 7 unused */
 } bang_search_stats;
 
 /* ---------------------------------------------------------------- errors */

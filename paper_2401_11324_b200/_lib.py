@@ -31,6 +31,7 @@ EXACT_DISTANCE = 4
 TABLE_GLOBAL = 8
 TABLE_SMEM = 16
 CODEBOOK_SMEM = 32
+PROFILE_PHASES = 64
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 
 _P = ctypes.c_void_p
@@ -47,10 +48,13 @@ class SearchStats(ctypes.Structure):
         ("ctas", ctypes.c_int32), ("adc_variant", ctypes.c_int32),
         ("kernel_ms", ctypes.c_float), ("table_ms", ctypes.c_float),
         ("algorithmic_bytes", ctypes.c_int64), ("adc_bytes", ctypes.c_int64),
+        ("phase_cycles", ctypes.c_int64 * 8),
     ]
 
     def as_dict(self):
-        return {name: getattr(self, name) for name, _ in self._fields_}
+        d = {name: getattr(self, name) for name, _ in self._fields_}
+        d["phase_cycles"] = list(d["phase_cycles"])
+        return d
 
 
 _SIGS = {

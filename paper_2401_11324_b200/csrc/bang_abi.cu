@@ -276,6 +276,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.adc_variant = pl.variant;
     p.rerank = (flags & BANG_RERANK) ? 1 : 0;
     p.debug = (flags & BANG_DEBUG_CHECKS) ? 1 : 0;
+    p.profile = (flags & BANG_PROFILE_PHASES) ? 1 : 0;
     p.smem_shared_bytes = pl.shared_bytes;
     p.per_warp_bytes = pl.per_warp;
     p.off_q = pl.off_q;
@@ -291,6 +292,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_tab = pl.off_tab;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
+    CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
     const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
     CU(cudaLaunchKernel(kfn, dim3(pl.ctas), dim3(pl.warps * 32), args, (size_t)pl.smem, st));
@@ -387,6 +389,7 @@ bang_status collect(bang_index *ix, unsigned long long *ctr) {
                           S.fresh * ix->m + S.rerank_cands * ix->dim * elem +
                           S.queries * (ix->dim * 4 + 16);
     S.adc_bytes = S.fresh * (ix->m + 12);
+    for (int i = 0; i < 8; ++i) S.phase_cycles[i] = (int64_t)ctr[kCtrPhase0 + i];
     ix->pending = false;
     return BANG_OK;
 }

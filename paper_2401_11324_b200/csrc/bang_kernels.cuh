@@ -26,7 +26,8 @@ enum Counter {
     kCtrOverflow = 5,
     kCtrDebugFail = 6,
     kCtrT0 = 7,
-    kCtrCount = 8,
+    kCtrPhase0 = 8,  // 8 slots of per-phase SM cycles (BANG_PROFILE_PHASES)
+    kCtrCount = 16,
 };
 
 // 24 warps x 32 lanes: leaves ptxas 80 registers per thread; shared memory
@@ -64,7 +65,7 @@ struct SearchParams {
     uint32_t medoid_p1, medoid_p2;
     unsigned long long *counters;
     // shapes
-    int32_t m, dim, R, medoid, k, t, vec_dtype, adc_variant, rerank, debug;
+    int32_t m, dim, R, medoid, k, t, vec_dtype, adc_variant, rerank, debug, profile;
     int32_t smem_shared_bytes, per_warp_bytes;
     int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
@@ -387,6 +388,21 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
         int iters = 0;
 
         for (;;) {
+            // phase profiler (flag BANG_PROFILE_PHASES): SM cycles per phase,
+            // summed over warps; the asm makes the wait for the prefetched
+            // adjacency row land in phase 0
+            long long t_ph = 0;
+#define BANG_PHASE(i)                                                               \
+    if (p.profile) {                                                                \
+        const long long now_ = clock64();                                           \
+        if (lane == 0) atomicAdd(p.counters + kCtrPhase0 + (i), (unsigned long long)(now_ - t_ph)); \
+        t_ph = now_;                                                                \
+    }
+            if (p.profile) {
+                t_ph = clock64();
+                asm volatile("" ::"r"(ids[0]), "r"(deg));
+                BANG_PHASE(0)
+            }
             // ---- expand u (engine.py:163-178)
             if (p.debug && lane == 0 && key_id(s_wl[upos]) != u)
                 atomicAdd(p.counters + kCtrDebugFail, 1ull);
@@ -406,8 +422,11 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                     if (lane + 32 * k < deg)
                         c0[k] = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)ids[k] * p.m));
             }
+            BANG_PHASE(1)
             BloomRow<NPL> br;
             bloom_issue<NPL>(bits, s_sum, p.geom, ids, deg, br);
+            if (p.profile) asm volatile("" ::"r"((int)br.fresh[0]));
+            BANG_PHASE(2)
             const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
             int F = 0, n_s = 0;
             if constexpr (MV > 0) {
@@ -416,6 +435,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                 if (p.adc_variant != kAdcExact) {
                     n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid, s_acc,
                                                       s_nk, s_tab, &F);
+                    BANG_PHASE(3)
                     if (bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br))
                         n_s = adc_fast_path<NPL, SUB, MV>(p, s_cb, s_q, qid, ids, br.fresh, c0, thr, s_fid,
                                                           s_acc, s_nk, s_tab, &F);
@@ -438,6 +458,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                     if (pass == 0 && !bloom_resolve<NPL>(bits, s_sum, p.geom, ids, deg, br)) break;
                 }
             }
+            BANG_PHASE(4)
             st_fresh += F;
             // ---- sort survivors; eager winner (engine.py:201-205)
             sort_keys(s_nk, n_s, s_sk);
@@ -460,6 +481,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
 #pragma unroll
                 for (int k = 0; k < NPL; ++k) nids[k] = 0u;
             }
+            BANG_PHASE(5)
             // ---- kernel 4: merge + truncate (engine.py:210-215)
             int first = 0;
             const int old_cnt = cnt;
@@ -472,6 +494,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
                 else wpos = hpos + lower_bound_u64(s_sk, n_s, head);
             }
             (void)old_cnt;
+            BANG_PHASE(6)
             if (wpos >= t) break;
             upos = wpos;
             if (p.debug && lane == 0 && s_wl[upos] != winner) atomicAdd(p.counters + kCtrDebugFail, 1ull);
