@@ -139,7 +139,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
     ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
-    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "codebook", "hbm-table"))
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-generic", "codebook", "hbm-table"))
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -225,8 +225,7 @@ def main():
         return
 
     # ---- device-resident timing (value)
-    flags = _lib.RERANK | {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
-                           "hbm-table": _lib.TABLE_GLOBAL}[args.variant]
+    flags = _lib.RERANK | searcher._ADC_FLAGS[args.variant]
     if args.phases:
         flags |= _lib.PROFILE_PHASES
     dev = torch.device("cuda", local)

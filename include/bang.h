@@ -52,6 +52,7 @@ typedef int32_t bang_status;
 #define BANG_TABLE_SMEM 16     /* ADC from a per-query table in shared memory         */
 #define BANG_CODEBOOK_SMEM 32  /* ADC recomputing entries from a CTA-shared codebook  */
 #define BANG_PROFILE_PHASES 64 /* accumulate per-phase cycles (diagnostics, slower)  */
+#define BANG_DEBUG_GENERIC 128 /* use the generic search kernel even where a specialised one exists */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 

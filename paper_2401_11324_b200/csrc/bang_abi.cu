@@ -16,6 +16,7 @@
 
 #include "../../include/bang.h"
 #include "bang_kernels.cuh"
+#include "bang_search_tab.cuh"
 
 using namespace bang;
 
@@ -122,6 +123,7 @@ namespace {
 struct Plan {
     int variant = kAdcSmemCodebook;
     int npl = 2, sub = 0, mv = 0;
+    bool tab_kernel = false;  // search_tab_kernel (smem table + 16-byte code rows)
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
     int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;
@@ -132,6 +134,22 @@ struct Plan {
 template <int NPL, int SUB, int MV>
 const void *kernel_ptr() {
     return reinterpret_cast<const void *>(&search_kernel<NPL, SUB, MV>);
+}
+
+template <int NPL, int SUB, int MV>
+const void *tab_kernel_ptr() {
+    return reinterpret_cast<const void *>(&search_tab_kernel<NPL, SUB, MV>);
+}
+
+const void *pick_tab_kernel(int npl, int sub, int mv) {
+#define BANG_T(N, S, V) \
+    if (npl == N && sub == S && mv == V) return tab_kernel_ptr<N, S, V>();
+    BANG_T(1, 4, 2) BANG_T(2, 4, 2) BANG_T(4, 4, 2)
+    BANG_T(1, 2, 3) BANG_T(2, 2, 3) BANG_T(4, 2, 3)
+    BANG_T(1, 0, 2) BANG_T(2, 0, 2) BANG_T(4, 0, 2)
+    BANG_T(1, 0, 3) BANG_T(2, 0, 3) BANG_T(4, 0, 3)
+#undef BANG_T
+    return nullptr;
 }
 
 const void *pick_kernel(int npl, int sub, int mv) {
@@ -201,7 +219,8 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     } else if (pl.variant == kAdcSmemTable) {
         pl.shared_bytes = 0;
         pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
-        pl.mv = pl.sub ? mv : 0;
+        pl.tab_kernel = mv > 0 && !(flags & BANG_DEBUG_GENERIC);
+        pl.mv = (pl.sub || pl.tab_kernel) ? mv : 0;
     } else {
         pl.shared_bytes = 0;
         pl.sub = 0;
@@ -209,9 +228,9 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     }
     int64_t w = (ix->max_smem - pl.shared_bytes) / pl.per_warp;
     if (w < 1) return fail(BANG_E_PARAM, "t=%d needs %d B of shared memory per query", t, pl.per_warp);
-    pl.warps = (int)std::min<int64_t>(kMaxSearchThreads / 32, w);
+    pl.warps = (int)std::min<int64_t>((pl.tab_kernel ? 256 : kMaxSearchThreads) / 32, w);
     pl.smem = pl.shared_bytes + pl.warps * pl.per_warp;
-    const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);
+    const void *kfn = pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv) : pick_kernel(pl.npl, pl.sub, pl.mv);
     if (!kfn) return fail(BANG_E_STATE, "no kernel instance for npl=%d sub=%d mv=%d", pl.npl, pl.sub, pl.mv);
     CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
     int per_sm = 0;
@@ -293,7 +312,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
-    const void *kfn = pick_kernel(pl.npl, pl.sub, pl.mv);
+    const void *kfn = pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv) : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
     CU(cudaLaunchKernel(kfn, dim3(pl.ctas), dim3(pl.warps * 32), args, (size_t)pl.smem, st));
     return BANG_OK;

@@ -279,7 +279,9 @@ class GraphSearcher(BaseEstimator):
         return self
 
     _ADC_FLAGS = {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
-                  "hbm-table": _lib.TABLE_GLOBAL}
+                  "hbm-table": _lib.TABLE_GLOBAL,
+                  # the smem table through the generic kernel (cross-check of the specialised one)
+                  "smem-table-generic": _lib.TABLE_SMEM | _lib.DEBUG_GENERIC}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):
