@@ -53,6 +53,7 @@ typedef int32_t bang_status;
 #define BANG_CODEBOOK_SMEM 32  /* ADC recomputing entries from a CTA-shared codebook  */
 #define BANG_PROFILE_PHASES 64 /* accumulate per-phase cycles (diagnostics, slower)  */
 #define BANG_DEBUG_GENERIC 128 /* use the generic search kernel even where a specialised one exists */
+#define BANG_WARP_PER_QUERY 256 /* smem-table ADC with one warp per query instead of one CTA */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 

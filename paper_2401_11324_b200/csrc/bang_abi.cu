@@ -17,6 +17,7 @@
 #include "../../include/bang.h"
 #include "bang_kernels.cuh"
 #include "bang_search_tab.cuh"
+#include "bang_search_cta.cuh"
 
 using namespace bang;
 
@@ -124,6 +125,8 @@ struct Plan {
     int variant = kAdcSmemCodebook;
     int npl = 2, sub = 0, mv = 0;
     bool tab_kernel = false;  // search_tab_kernel (smem table + 16-byte code rows)
+    bool cta_kernel = false;  // search_cta_kernel (one CTA per query, smem table)
+    int nt = 0;               // threads per CTA of the CTA kernel
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
     int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;
@@ -149,6 +152,22 @@ const void *pick_tab_kernel(int npl, int sub, int mv) {
     BANG_T(1, 0, 2) BANG_T(2, 0, 2) BANG_T(4, 0, 2)
     BANG_T(1, 0, 3) BANG_T(2, 0, 3) BANG_T(4, 0, 3)
 #undef BANG_T
+    return nullptr;
+}
+
+template <int NT, int SUB, int MV>
+const void *cta_kernel_ptr() {
+    return reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV>);
+}
+
+const void *pick_cta_kernel(int nt, int sub, int mv) {
+#define BANG_C(N, S, V) \
+    if (nt == N && sub == S && mv == V) return cta_kernel_ptr<N, S, V>();
+    BANG_C(64, 4, 2) BANG_C(128, 4, 2) BANG_C(256, 4, 2)
+    BANG_C(64, 2, 3) BANG_C(128, 2, 3) BANG_C(256, 2, 3)
+    BANG_C(64, 0, 2) BANG_C(128, 0, 2) BANG_C(256, 0, 2)
+    BANG_C(64, 0, 3) BANG_C(128, 0, 3) BANG_C(256, 0, 3)
+#undef BANG_C
     return nullptr;
 }
 
@@ -219,12 +238,44 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     } else if (pl.variant == kAdcSmemTable) {
         pl.shared_bytes = 0;
         pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
-        pl.tab_kernel = mv > 0 && !(flags & BANG_DEBUG_GENERIC);
-        pl.mv = (pl.sub || pl.tab_kernel) ? mv : 0;
+        pl.cta_kernel = mv > 0 && !(flags & (BANG_DEBUG_GENERIC | BANG_WARP_PER_QUERY)) &&
+                        t <= 4 * 2 * rpad;
+        pl.tab_kernel = mv > 0 && !pl.cta_kernel && !(flags & BANG_DEBUG_GENERIC);
+        pl.mv = (pl.sub || pl.tab_kernel || pl.cta_kernel) ? mv : 0;
     } else {
         pl.shared_bytes = 0;
         pl.sub = 0;
         pl.mv = pl.variant == kAdcGlobalTable ? mv : 0;
+    }
+    if (pl.cta_kernel) {
+        // one CTA per query: 2 threads per neighbour slot; CTA-private layout
+        pl.nt = 2 * rpad;
+        int off = 0;
+        auto take = [&](int64_t bytes) { const int o = off; off += (int)align_up(bytes, 16); return o; };
+        pl.off_q = take(4LL * ix->dim);
+        pl.off_wl = take(8LL * t);
+        pl.off_sk = take(8LL * rpad);
+        pl.off_nk = take(8LL * rpad);
+        pl.off_fid = take(4LL * rpad);
+        pl.off_alive = take(rpad);
+        pl.off_acc = take(256);  // CtaMisc
+        pl.off_vis = take(t);
+        pl.off_sum = take(4LL * pl.sum_words);
+        pl.off_tab = take(tab_bytes);
+        pl.per_warp = off;  // bytes per CTA
+        pl.shared_bytes = 0;
+        pl.warps = pl.nt / 32;
+        pl.smem = pl.per_warp;
+        if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
+        const void *kc = pick_cta_kernel(pl.nt, pl.sub, pl.mv);
+        if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
+        CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, pl.nt, pl.smem));
+        if (per_sm < 1) return fail(BANG_E_CUDA, "search CTA cannot be resident");
+        pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, nq));
+        pl.slots = pl.ctas;
+        return BANG_OK;
     }
     int64_t w = (ix->max_smem - pl.shared_bytes) / pl.per_warp;
     if (w < 1) return fail(BANG_E_PARAM, "t=%d needs %d B of shared memory per query", t, pl.per_warp);
@@ -312,7 +363,9 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
-    const void *kfn = pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv) : pick_kernel(pl.npl, pl.sub, pl.mv);
+    const void *kfn = pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
+                                      : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
     CU(cudaLaunchKernel(kfn, dim3(pl.ctas), dim3(pl.warps * 32), args, (size_t)pl.smem, st));
     return BANG_OK;

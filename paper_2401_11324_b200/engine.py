@@ -281,7 +281,9 @@ class GraphSearcher(BaseEstimator):
     _ADC_FLAGS = {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
                   "hbm-table": _lib.TABLE_GLOBAL,
                   # the smem table through the generic kernel (cross-check of the specialised one)
-                  "smem-table-generic": _lib.TABLE_SMEM | _lib.DEBUG_GENERIC}
+                  "smem-table-generic": _lib.TABLE_SMEM | _lib.DEBUG_GENERIC,
+                  # the smem table with one warp (not one CTA) per query
+                  "smem-table-warp": _lib.TABLE_SMEM | _lib.WARP_PER_QUERY}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):

@@ -302,7 +302,7 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
                     adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
                     k=10, t=t, bloom_entries=399_887, threads=8)
-    for variant in ("auto", "smem-table", "smem-table-generic", "codebook", "hbm-table"):
+    for variant in ("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table"):
         res = s.set_adc_variant(variant).search(q)
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
