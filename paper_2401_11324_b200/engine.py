@@ -73,6 +73,27 @@ class VisitLogs(Sequence):
     def __eq__(self, other):
         return len(self) == len(other) and all(np.array_equal(a, b) for a, b in zip(self, other))
 
+    @classmethod
+    def concat(cls, logs_list) -> "VisitLogs":
+        """Logs of several batches/shards, in order (plain lists accepted)."""
+        out = cls([])
+        for logs in logs_list:
+            if isinstance(logs, VisitLogs):
+                for offs, flat in zip(logs._offs, logs._flat):
+                    out._offs.append(offs)
+                    out._flat.append(flat)
+                    out._base.append(out._base[-1] + len(offs) - 1)
+            else:
+                arrs = [np.asarray(a, np.int64) for a in logs]
+                offs = np.zeros(len(arrs) + 1, np.int64)
+                if arrs:
+                    offs[1:] = np.cumsum([a.size for a in arrs])
+                flat = np.concatenate(arrs) if arrs else np.zeros(0, np.int64)
+                out._offs.append(offs)
+                out._flat.append(flat)
+                out._base.append(out._base[-1] + len(arrs))
+        return out
+
 
 @dataclass
 class SearchResult:
@@ -270,7 +291,10 @@ class GraphSearcher(BaseEstimator):
         old = getattr(self, "index_", None)
         if old is not None:
             old.close()
-        self.index_ = DeviceIndex(graph, base, codebook, codes, placement)
+        # ``device`` (not a constructor parameter): the GPU this replica uses
+        # (sharding.ShardedSearcher sets one per replica); default BANG_DEVICE/LOCAL_RANK
+        self.index_ = DeviceIndex(graph, base, codebook, codes, placement,
+                                  device=getattr(self, "device", None))
         self.host_ = IndexHost(graph, base)
         self.graph_ = graph
         self.codebook_ = codebook
