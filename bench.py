@@ -1,9 +1,9 @@
 """Benchmark of the B200 batched graph search (BASELINE.json metric).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config C2]
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config C3]
 
-One "step" = one batched search of the config's query batch (10K queries at
-C2) at the smallest worklist size t whose recall@10 >= 0.9 (chosen by a
+One "step" = one batched search of the config's query batch (10K queries; the
+default config is C3, BASELINE.json's 10M-point target) at the smallest worklist size t whose recall@10 >= 0.9 (chosen by a
 sweep before timing).  Reported:
   value  QPS with queries/outputs resident in HBM (bang_search_device), the
          sum of per-step CUDA-event times on the launching stream, L2 flushed
@@ -33,7 +33,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-T_SWEEP = (10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 128, 160, 200)
+T_SWEEP = (10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 112, 128, 144, 160, 176, 200, 224, 256)
 
 
 def log(*a):
@@ -131,7 +131,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--config", default=os.environ.get("BANG_BENCH_CONFIG", "C2"))
+    ap.add_argument("--config", default=os.environ.get("BANG_BENCH_CONFIG", "C3"))
     ap.add_argument("--t", type=int, default=0, help="fixed worklist size (default: recall sweep)")
     ap.add_argument("--target-recall", type=float, default=0.9)
     ap.add_argument("--bloom", type=int, default=399_887)
@@ -151,19 +151,31 @@ def main():
     import torch.distributed as dist
     if world > 1:
         torch.cuda.set_device(local) if torch.cuda.is_available() else None
+        import datetime
+        # rank 0 builds the artifacts (minutes at C3) while the others wait
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo",
-                                init_method="env://")
+                                init_method="env://", timeout=datetime.timedelta(minutes=45))
     if args.impl == "reference" and rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
     from paper_2401_11324_b200 import GraphSearcher, _lib, set_device
-    from paper_2401_11324_b200.tools.bench_data import CONFIGS, build_artifacts
+    from paper_2401_11324_b200.tools.bench_data import CONFIGS, EXACT_KNN_LIMIT, build_artifacts
     set_device(local)
     nq = CONFIGS[args.config][1]
     # each rank owns its own nq-query shard (weak scaling)
-    art = build_artifacts(args.config, seed=0, nq_total=nq * world, cache_dir=args.cache or None, log=log)
+    if world > 1:
+        # one build per box: rank 0 writes the memory-mapped cache, the others map it
+        cache = args.cache or "/tmp/bang_bench_cache"
+        if rank == 0:
+            art = build_artifacts(args.config, seed=0, nq_total=nq * world, cache_dir=cache, log=log)
+        dist.barrier()
+        if rank != 0:
+            art = build_artifacts(args.config, seed=0, nq_total=nq * world, cache_dir=cache, log=log,
+                                  load_only=True)
+    else:
+        art = build_artifacts(args.config, seed=0, nq_total=nq * world, cache_dir=args.cache or None, log=log)
     lo, hi = rank * nq, (rank + 1) * nq
     shard = dict(art)
     shard["queries"] = art["queries"][lo:hi]
@@ -198,7 +210,10 @@ def main():
     config = {"workload": args.config, "desc": meta["desc"], "n": meta["n"], "dim": meta["dim"],
               "vectors": meta["dtype"], "R": meta["R"], "m": meta["m"], "k": k, "t": t_sel,
               "queries_per_gpu": nq, "bloom_entries": args.bloom, "mode": "in_memory",
-              "graph": "GPU kNN(2R) + RobustPrune(1.2) + reverse edges (tools/graph_build.py)",
+              "graph": ("GPU kNN(2R) + RobustPrune(1.2) + reverse edges (tools/graph_build.py)"
+                        if meta["n"] <= EXACT_KNN_LIMIT else
+                        "GPU IVF kNN(2R) + RobustPrune(1.2) + reverse edges, then one search-based Vamana "
+                        "pass (t=64) with this search (tools/graph_build.py)"),
               "l2": "flushed between steps (256 MiB memset outside the step events)",
               "parallelism": f"query-sharded x{world}, index replicated, no collective"}
 
@@ -351,8 +366,13 @@ def main():
     if args.phases:
         pc = s_last["phase_cycles"]
         it = max(1, s_last["iterations"])
-        names = ["adj_wait", "expand", "bloom_issue", "adc", "bloom_resolve", "sort_eager_prefetch", "merge"]
-        out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
+        if s_last["slots"] == s_last["ctas"]:  # search_cta_kernel: thread 0's cycles
+            names = ["bloom_load", "zero_sync", "adc_reduce", "coll_sync", "winner_prefetch", "sort", "merge"]
+            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
+            out["phase_cycles_per_iteration"]["epilogue_per_query"] = round(pc[7] / max(1, nq), 1)
+        else:
+            names = ["adj_wait", "expand", "bloom_issue", "adc", "bloom_resolve", "sort_eager_prefetch", "merge"]
+            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

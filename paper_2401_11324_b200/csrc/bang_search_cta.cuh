@@ -29,7 +29,10 @@ struct CtaMisc {
     int hpos;
     int coll;
     unsigned long long head;
+    unsigned long long ph[8];  // phase profiler: thread 0's cycles per phase
+    long long t_ph;
 };
+static_assert(sizeof(CtaMisc) <= 256, "CtaMisc must fit its 256-byte smem slot");
 
 template <int NT, int SUB, int MV>
 // 768/NT CTAs per SM: 6 queries of 128 threads (R <= 64) fit the register file at <= 80 regs
@@ -60,6 +63,16 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
     const uint64_t hseed = h ? kFnvOffsetH2 : kFnvOffset;
 
     unsigned long long st_iters = 0, st_probes = 0, st_fresh = 0, st_rr = 0;
+    // phase profiler (BANG_PROFILE_PHASES): thread 0's SM cycles per phase,
+    // kept in shared memory so the option costs no registers
+    if (tid == 0)
+        for (int i = 0; i < 8; ++i) s_m->ph[i] = 0;
+#define BANG_CTA_PHASE(i)                                      \
+    if (p.profile && tid == 0) {                               \
+        const long long now_ = clock64();                      \
+        s_m->ph[i] += (unsigned long long)(now_ - s_m->t_ph);  \
+        s_m->t_ph = now_;                                      \
+    }
 
     for (;;) {
         if (tid == 0) s_m->qi = (long long)atomicAdd(p.counters + kCtrNextQuery, 1ull);
@@ -123,6 +136,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
         __syncthreads();
 
         for (;;) {
+            if (p.profile && tid == 0) s_m->t_ph = clock64();
             // ---- expand u (engine.py:163-178); warp 0 finds the next unvisited
             // entry after u (the eager "head")
             if (warp == 0) {
@@ -166,6 +180,8 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
                 if (init) word = __ldcg(bits + (ps >> 5));
             }
             const uint32_t mybit = (word >> (ps & 31)) & 1u;
+            if (p.profile) asm volatile("" ::"r"(mybit), "r"(cw[0]));
+            BANG_CTA_PHASE(0)
             const uint32_t pbit = __shfl_xor_sync(kFull, mybit, 1);
             const uint32_t pps = __shfl_xor_sync(kFull, ps, 1);
             bool fresh = valid && !(mybit && pbit);
@@ -176,6 +192,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
                 sum_set(s_sum, ps >> 5);
             }
             __syncthreads();  // zeroing stores (any warp) before any atomic; publishes head
+            BANG_CTA_PHASE(1)
             uint32_t old = 0;
             const bool do_atom = fresh && !(h == 1 && pps == ps);
             if (do_atom) old = atomicOr(bits + (ps >> 5), 1u << (ps & 31));
@@ -223,7 +240,10 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
                     s_m->wcnt[warp] = __popc(sb);
                     s_m->wfresh[warp] = __popc(fb);
                 }
-                if (__syncthreads_or(coll)) {
+                BANG_CTA_PHASE(2)
+                const int any_coll = __syncthreads_or(coll);
+                BANG_CTA_PHASE(3)
+                if (any_coll) {
                     // in-row slot sharing: restore the pre-state, replay in order
                     if (fresh) {
                         if (init) __stcg(bits + (ps >> 5), word);
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
             const unsigned sball = __ballot_sync(kFull, surv);
             if (surv) s_nk[woff + __popc(sball & lt)] = key;
             __syncthreads();
+            BANG_CTA_PHASE(4)
             for (int q = tid; q < n; q += NT) {
                 const uint64_t k = s_nk[q];
                 int r = 0, i = 0;
@@ -293,6 +314,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
                 s_sk[r] = k;
             }
             __syncthreads();
+            BANG_CTA_PHASE(5)
             // ---- kernel 4b: merge + truncate to t (engine.py:210-215)
             int wpos = t;
             if (winner != kSentinel)
@@ -335,6 +357,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
             }
             cnt = min(t, cnt + n);
             __syncthreads();
+            BANG_CTA_PHASE(6)
             // ---- converge (engine.py:217-236)
             if (wpos >= t) break;
             upos = wpos;
@@ -344,6 +367,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
             id = nid;
         }
         st_iters += iters;
+        if (p.profile && tid == 0) s_m->t_ph = clock64();
 
         // ---- outputs (engine.py:244-269)
         int32_t *oid = p.out_ids + qid * p.k;
@@ -392,6 +416,12 @@ __global__ void __launch_bounds__(NT, 768 / NT) search_cta_kernel(const SearchPa
             if (tid == 0) p.out_short[qid] = cnt < p.k;
         }
         __syncthreads();
+        BANG_CTA_PHASE(7)
+    }
+#undef BANG_CTA_PHASE
+    if (p.profile && tid == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicAdd(p.counters + kCtrPhase0 + i, s_m->ph[i]);
     }
     if (tid == 0) {
         atomicAdd(p.counters + kCtrIterations, st_iters);

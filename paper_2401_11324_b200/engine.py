@@ -73,6 +73,17 @@ class VisitLogs(Sequence):
     def __eq__(self, other):
         return len(self) == len(other) and all(np.array_equal(a, b) for a, b in zip(self, other))
 
+    def csr(self):
+        """(offsets (n+1,) int64, ids int64): all logs as one CSR pair."""
+        if len(self._offs) == 1:
+            return self._offs[0], self._flat[0]
+        offs, flats, base = [np.zeros(1, np.int64)], [], 0
+        for o, f in zip(self._offs, self._flat):
+            offs.append(o[1:] - o[0] + base)
+            flats.append(f[o[0]:o[-1]])
+            base += int(o[-1] - o[0])
+        return np.concatenate(offs), (np.concatenate(flats) if flats else np.zeros(0, np.int64))
+
     @classmethod
     def concat(cls, logs_list) -> "VisitLogs":
         """Logs of several batches/shards, in order (plain lists accepted)."""

@@ -31,56 +31,124 @@ CONFIGS = {
 }
 
 
+EXACT_KNN_LIMIT = 2_000_000
+# search-based Vamana passes after the partitioned k-NN graph (n > EXACT_KNN_LIMIT):
+# (passes, worklist t).  At C3 two t=128 passes lift recall@10 at t=200 from
+# 0.846 to 0.915 (profiles/r01/c3_graph_study.jsonl).
+REFINE = (2, 128)
+
+
+def refine_with_search(base, graph, codebook, codes, R, t=64, sigma=1.2, chunk=1 << 20, log=print):
+    """graph_build.refine_graph with visit logs from GraphSearcher (t=64)."""
+    import torch
+    from .._dev import torch_device
+    from ..engine import GraphSearcher
+    from .graph_build import refine_graph
+    dev = torch_device()
+    s = GraphSearcher(k=10, t=t, mode="in_memory", batch_size=chunk)
+    s.fit(base, graph=graph, codebook=codebook, codes=codes)
+
+    def visit_fn(lo, hi):
+        return s.search(base[lo:hi]).visit_logs.csr()
+
+    x = torch.from_numpy(np.ascontiguousarray(base, np.float32)).to(dev)
+    adj = torch.from_numpy(graph.adjacency).to(dev).long()
+    deg = torch.from_numpy(graph.degrees).to(dev).long()
+    adj, deg = refine_graph(x, adj, deg, visit_fn, R, sigma, chunk=chunk, log=log)
+    del s
+    adj_np = adj.to(torch.int32).cpu().numpy()
+    deg_np = deg.to(torch.int32).cpu().numpy()
+    adj_np[np.arange(R)[None, :] >= deg_np[:, None]] = -1
+    return GraphIndex(adj_np, deg_np, graph.medoid, R, validate=False)
+
+
 def _key(name, seed, nq_total):
-    return hashlib.sha1(f"v2|{name}|{CONFIGS[name]}|{seed}|{nq_total}".encode()).hexdigest()[:16]
+    return hashlib.sha1(f"v3|{name}|{CONFIGS[name]}|{REFINE}|{seed}|{nq_total}".encode()).hexdigest()[:16]
+
+
+_ARRAYS = ("base", "queries", "adjacency", "degrees", "medoid", "sub_sizes", "centroids", "codes",
+           "gt_ids", "gt_dists")
+
+
+def cache_path(name: str, seed: int, nq_total: int, cache_dir: str) -> str:
+    return os.path.join(cache_dir, f"bang_{name}_{_key(name, seed, nq_total)}")
+
+
+def _load_cached(path, name, meta, log):
+    """Arrays are memory-mapped .npy files: ranks on one box share the page cache."""
+    d = {k: np.load(os.path.join(path, k + ".npy"), mmap_mode="r") for k in _ARRAYS}
+    R = meta["R"]
+    sizes = [int(s) for s in d["sub_sizes"]]
+    cents, pos = [], 0
+    cat = np.asarray(d["centroids"])
+    for s in sizes:
+        cents.append(cat[pos:pos + 256 * s].reshape(256, s))
+        pos += 256 * s
+    log(f"[bench_data] {name}: loaded cached artifacts {path}")
+    return dict(base=d["base"], queries=np.asarray(d["queries"]),
+                graph=GraphIndex(d["adjacency"], np.asarray(d["degrees"]), int(d["medoid"]), R, validate=False),
+                codebook=PQCodebook(dim=meta["dim"], subspace_sizes=sizes, centroids=cents),
+                codes=CompressedVectors(d["codes"]), gt_ids=np.asarray(d["gt_ids"]),
+                gt_dists=np.asarray(d["gt_dists"]), meta=meta)
+
+
+def _save_cached(path, arrays, log):
+    tmp = path + ".tmp"
+    try:
+        os.makedirs(tmp, exist_ok=True)
+        for k in _ARRAYS:
+            np.save(os.path.join(tmp, k + ".npy"), np.asarray(arrays[k]))
+        os.replace(tmp, path)
+    except OSError as e:  # a full scratch disk only costs the cache
+        log(f"[bench_data] cache not written ({e})")
+        import shutil
+        shutil.rmtree(tmp, ignore_errors=True)
 
 
 def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache_dir: str | None = None,
-                    log=print):
-    """Returns dict(base, queries, graph, codebook, codes, gt_ids, gt_dists, meta)."""
+                    log=print, load_only: bool = False):
+    """Returns dict(base, queries, graph, codebook, codes, gt_ids, gt_dists, meta).
+    load_only: the caller knows another process has written the cache."""
     from .graph_build import build_graph
     from .groundtruth import brute_force_knn
     from .pq_train import encode, train_codebook
 
     n, nq, dim, dt, clusters, R, m, desc = CONFIGS[name]
     nq_total = nq_total or nq
+    meta = dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters)
     path = None
     if cache_dir:
         os.makedirs(cache_dir, exist_ok=True)
-        path = os.path.join(cache_dir, f"bang_{name}_{_key(name, seed, nq_total)}.npz")
-        if os.path.exists(path):
-            with np.load(path) as z:
-                d = {k: z[k] for k in z.files}
-            sizes = [int(s) for s in d["sub_sizes"]]
-            cents, pos = [], 0
-            for s in sizes:
-                cents.append(d["centroids"][pos:pos + 256 * s].reshape(256, s))
-                pos += 256 * s
-            log(f"[bench_data] {name}: loaded cached artifacts {path}")
-            return dict(base=d["base"], queries=d["queries"],
-                        graph=GraphIndex(d["adjacency"], d["degrees"], int(d["medoid"]), R, validate=False),
-                        codebook=PQCodebook(dim=dim, subspace_sizes=sizes, centroids=cents),
-                        codes=CompressedVectors(d["codes"]), gt_ids=d["gt_ids"], gt_dists=d["gt_dists"],
-                        meta=dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters))
+        path = cache_path(name, seed, nq_total, cache_dir)
+        if os.path.isdir(path) or load_only:
+            return _load_cached(path, name, meta, log)
     t0 = time.time()
     base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed)
     if dt == "u8":
         base, queries = to_u8(base), to_u8(queries).astype(np.float32)
     t1 = time.time()
-    graph = build_graph(base, degree_bound=R, seed=seed)
+    graph = build_graph(base, degree_bound=R, seed=seed, log=log)
     t2 = time.time()
     cb = train_codebook(base, m=m, iters=15, seed=seed)
     codes = encode(base, cb)
     t3 = time.time()
+    if n > EXACT_KNN_LIMIT:
+        # partitioned k-NN graph -> one search-based Vamana pass with the
+        # B200 search itself (the reference's builder, graph.py:251-344,
+        # inserts by greedy search too)
+        for _ in range(REFINE[0]):
+            graph = refine_with_search(base, graph, cb, codes, R, t=REFINE[1], log=log)
+        t2 += time.time() - t3
+        t3 = time.time()
     gt_ids, gt_d = brute_force_knn(base, queries, 10)
     t4 = time.time()
     log(f"[bench_data] {name}: data {t1 - t0:.1f}s graph {t2 - t1:.1f}s pq {t3 - t2:.1f}s gt {t4 - t3:.1f}s"
         f" (mean degree {graph.degrees.mean():.1f})")
     if path:
-        tmp = path + ".tmp.npz"
-        np.savez(tmp, base=base, queries=queries, adjacency=graph.adjacency, degrees=graph.degrees,
-                 medoid=np.int64(graph.medoid), sub_sizes=np.asarray(cb.subspace_sizes, np.int32),
-                 centroids=cb.concatenated(), codes=codes.codes, gt_ids=gt_ids, gt_dists=gt_d)
-        os.replace(tmp, path)
+        _save_cached(path, dict(base=base, queries=queries, adjacency=graph.adjacency, degrees=graph.degrees,
+                                medoid=np.int64(graph.medoid),
+                                sub_sizes=np.asarray(cb.subspace_sizes, np.int32),
+                                centroids=cb.concatenated(), codes=codes.codes, gt_ids=gt_ids,
+                                gt_dists=gt_d), log)
     return dict(base=base, queries=queries, graph=graph, codebook=cb, codes=codes, gt_ids=gt_ids,
-                gt_dists=gt_d, meta=dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters))
+                gt_dists=gt_d, meta=meta)

@@ -14,10 +14,17 @@ def gaussian_mixture(n: int, n_queries: int, dim: int, clusters: int = 32, seed:
     axis = (np.arange(dim) + 1.0) ** -float(spectrum_decay)
     centers = rng.normal(0.0, center_scale, size=(clusters, dim)) * axis
 
-    def draw(count: int) -> np.ndarray:
+    def draw(count: int, chunk: int = 1 << 20) -> np.ndarray:
+        # the normal stream is consumed in row order, so filling the output
+        # chunk by chunk yields the reference's values with a bounded f64
+        # working set (a 10M x 96 draw would otherwise need ~25 GB)
         which = rng.integers(0, clusters, size=count)
-        noise = rng.normal(0.0, cluster_scale, size=(count, dim)) * axis
-        return (centers[which] + noise).astype(np.float32)
+        out = np.empty((count, dim), np.float32)
+        for lo in range(0, count, chunk):
+            hi = min(count, lo + chunk)
+            noise = rng.normal(0.0, cluster_scale, size=(hi - lo, dim)) * axis
+            out[lo:hi] = centers[which[lo:hi]] + noise
+        return out
 
     base = draw(n)
     queries = draw(n_queries) if n_queries else np.zeros((0, dim), np.float32)

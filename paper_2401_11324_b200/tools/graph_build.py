@@ -52,35 +52,37 @@ def knn(x, K: int, qchunk: int = 1024, bchunk: int = 1 << 21):
     return out_i, out_d
 
 
-def robust_prune(x, cand, dcand, R: int, sigma: float, chunk: int = 8192):
+def robust_prune(x, cand, dcand, R: int, sigma: float, chunk: int = 0):
     """Batched RobustPrune (graph.py:118-147) over candidate rows sorted by
-    (distance, id); cand -1 = empty.  Returns (n, R) ids (-1 padded), degrees."""
+    (distance, id); cand -1 = empty.  Returns (n, R) ids (-1 padded), degrees.
+    The per-rank loop is sync-free (masked scatter), so a chunk costs a fixed
+    number of launches whatever its contents."""
     import torch
     n, C = cand.shape
     sig2 = float(sigma) ** 2
+    if not chunk:
+        chunk = max(1024, min(32768, (1 << 31) // max(1, C * C * 4)))
     out = torch.full((n, R), -1, dtype=torch.int64, device=x.device)
     deg = torch.zeros(n, dtype=torch.int64, device=x.device)
     for lo in range(0, n, chunk):
-        c = cand[lo:lo + chunk]
+        c = cand[lo:lo + chunk].long()
         dp = dcand[lo:lo + chunk]
         B = c.shape[0]
         alive = c >= 0
-        v = x[c.clamp_min(0)]  # (B, C, d)
+        v = x[c.clamp_min(0)].float()  # (B, C, d)
         vsq = v.square().sum(-1)
         D = vsq[:, :, None] + vsq[:, None, :] - 2.0 * torch.bmm(v, v.transpose(1, 2))
+        del v
         kept = torch.full((B, R), -1, dtype=torch.int64, device=x.device)
         nk = torch.zeros(B, dtype=torch.int64, device=x.device)
-        ar = torch.arange(B, device=x.device)
-        for r in range(C):
+        last = int((alive.sum(0) > 0).nonzero().max().item()) + 1 if bool(alive.any()) else 0
+        for r in range(last):
             take = alive[:, r] & (nk < R)
-            if not bool(take.any()):
-                if not bool(alive[:, r + 1:].any()):
-                    break
-                continue
-            kept[ar[take], nk[take]] = c[take, r]
+            slot = nk.clamp_max(R - 1)[:, None]
+            cur = kept.gather(1, slot).squeeze(1)
+            kept.scatter_(1, slot, torch.where(take, c[:, r], cur)[:, None])
             nk += take.long()
-            kill = take[:, None] & (sig2 * D[:, r, :] <= dp)
-            alive &= ~kill
+            alive &= ~(take[:, None] & (sig2 * D[:, r, :] <= dp))
             alive[:, r] = False
         out[lo:lo + B] = kept
         deg[lo:lo + B] = nk
@@ -96,6 +98,15 @@ def _sort_rows_by_dist(ids, d):
     return torch.gather(ids, 1, o2), torch.gather(d, 1, o2)
 
 
+def _pair_sqdist(x, a, b, chunk: int = 1 << 23):
+    """|x[a] - x[b]|^2 for index vectors a, b, in bounded chunks."""
+    import torch
+    out = torch.empty(a.shape[0], dtype=torch.float32, device=x.device)
+    for lo in range(0, a.shape[0], chunk):
+        out[lo:lo + chunk] = (x[a[lo:lo + chunk]].float() - x[b[lo:lo + chunk]].float()).square().sum(1)
+    return out
+
+
 def add_reverse_edges(x, adj, deg, R: int, sigma: float, rev_cap: int | None = None):
     """For every edge p->q offer p to q; rows that overflow R are re-pruned."""
     import torch
@@ -104,12 +115,14 @@ def add_reverse_edges(x, adj, deg, R: int, sigma: float, rev_cap: int | None = N
     valid = adj >= 0
     src = torch.arange(n, device=x.device)[:, None].expand_as(adj)[valid]
     dst = adj[valid]
-    dd = (x[src] - x[dst]).square().sum(1)
-    # group by destination, nearest sources first
-    order = torch.argsort(dd, stable=True)
+    dd = _pair_sqdist(x, src, dst)
+    # group by destination, nearest sources first; one stable sort on the
+    # (dst, f32 bits of dd) key == stable sort by dd, then stable by dst
+    key = (dst << 32) | dd.view(torch.int32).long()
+    order = torch.sort(key, stable=True).indices
+    del key
     src, dst, dd = src[order], dst[order], dd[order]
-    order = torch.argsort(dst, stable=True)
-    src, dst, dd = src[order], dst[order], dd[order]
+    del order
     counts = torch.bincount(dst, minlength=n)
     starts = torch.cumsum(counts, 0) - counts
     rank = torch.arange(dst.numel(), device=x.device) - starts[dst]
@@ -118,15 +131,19 @@ def add_reverse_edges(x, adj, deg, R: int, sigma: float, rev_cap: int | None = N
     revd = torch.full((n, rev_cap), float("inf"), device=x.device)
     rev[dst[keep], rank[keep]] = src[keep]
     revd[dst[keep], rank[keep]] = dd[keep]
-    own_d = torch.where(valid, (x[adj.clamp_min(0)] - x[:, None, :]).square().sum(-1),
-                        torch.full_like(adj, float("inf"), dtype=torch.float32))
+    del src, dst, dd, rank, keep
+    own_d = torch.full(adj.shape, float("inf"), dtype=torch.float32, device=x.device)
+    rows = torch.arange(n, device=x.device)[:, None].expand_as(adj)
+    own_d[valid] = _pair_sqdist(x, rows[valid], adj[valid])
     cand = torch.cat([adj, rev], 1)
     cd = torch.cat([own_d, revd], 1)
+    del rev, revd, own_d
     # drop duplicates (mutual edges): keep one copy per id
     cs, o = torch.sort(cand, dim=1)
     dup = torch.zeros_like(cs, dtype=torch.bool)
     dup[:, 1:] = (cs[:, 1:] == cs[:, :-1]) & (cs[:, 1:] >= 0)
     dup = torch.zeros_like(dup).scatter_(1, o, dup)
+    del cs, o
     cand = torch.where(dup, torch.full_like(cand, -1), cand)
     cd = torch.where(dup | (cand < 0), torch.full_like(cd, float("inf")), cd)
     cand = torch.where(torch.isinf(cd), torch.full_like(cand, -1), cand)
@@ -144,11 +161,103 @@ def add_reverse_edges(x, adj, deg, R: int, sigma: float, rev_cap: int | None = N
     return new_adj, new_deg
 
 
-def build_graph(base, degree_bound: int = 64, build_worklist: int = 200, sigma: float = 1.2,
-                seed: int = 0, candidates: int | None = None) -> GraphIndex:
-    """k-NN candidates (2R by default) -> RobustPrune(sigma) -> reverse edges."""
+def _nearest_centroids(x, cent, k: int, chunk: int = 1 << 18):
+    """ids (n, k) of the k nearest rows of cent for every row of x (f32)."""
     import torch
-    dev = torch_device()
+    csq = cent.square().sum(1)
+    out = torch.empty((x.shape[0], k), dtype=torch.int64, device=x.device)
+    for lo in range(0, x.shape[0], chunk):
+        xb = x[lo:lo + chunk].float()
+        d = csq[None, :] - 2.0 * (xb @ cent.T)
+        out[lo:lo + chunk] = torch.topk(d, k, dim=1, largest=False).indices
+    return out
+
+
+def kmeans(x, nlist: int, iters: int = 10, sample: int = 1 << 20, seed: int = 0):
+    """Lloyd k-means on a seeded sample (partitioning for the IVF k-NN)."""
+    import torch
+    n = x.shape[0]
+    g = torch.Generator().manual_seed(seed)
+    idx = torch.randperm(n, generator=g)[:min(n, max(sample, nlist))].to(x.device)
+    xs = x[idx].float()
+    cent = xs[torch.randperm(xs.shape[0], generator=g)[:nlist].to(x.device)].clone()
+    for _ in range(iters):
+        a = _nearest_centroids(xs, cent, 1)[:, 0]
+        sums = torch.zeros_like(cent).index_add_(0, a, xs)
+        cnt = torch.bincount(a, minlength=nlist).float()
+        cent = torch.where(cnt[:, None] > 0, sums / cnt.clamp_min(1)[:, None], cent)
+    return cent
+
+
+def knn_ivf(x, K: int, nlist: int = 0, nprobe: int = 8, max_rows: int = 4096, seed: int = 0):
+    """Approximate K-NN of every row (self excluded) in O(n * nprobe * n/nlist):
+    k-means partitions; the rows of partition c are compared exactly (f32)
+    against every row of the nprobe partitions whose centroids are nearest
+    to c's.  Returns ids (n, K) int64 (-1 where fewer candidates) and squared
+    distances (inf there).  Sub-quadratic replacement of knn() for the 10M+
+    configs; graph construction only, not the hot path."""
+    import torch
+    n = x.shape[0]
+    K = min(K, n - 1)
+    nlist = nlist or max(1, min(n // 64, int(round(n / 1000))))
+    nprobe = min(nprobe, nlist)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        cent = kmeans(x, nlist, seed=seed)
+        assign = _nearest_centroids(x, cent, 1)[:, 0]
+        probes = _nearest_centroids(cent, cent, nprobe).cpu().numpy()
+        order = torch.argsort(assign, stable=True)
+        counts = torch.bincount(assign, minlength=nlist).cpu().numpy()
+        offs = np.concatenate([[0], np.cumsum(counts)])
+        sq = x.float().square().sum(1)
+        out_i = torch.full((n, K), -1, dtype=torch.int64, device=x.device)
+        out_d = torch.full((n, K), float("inf"), dtype=torch.float32, device=x.device)
+        for c in range(nlist):
+            if counts[c] == 0:
+                continue
+            cand = torch.cat([order[offs[p]:offs[p + 1]] for p in probes[c] if counts[p]])
+            xc = x[cand].float()
+            kk = min(K, cand.shape[0] - 1)
+            if kk < 1:
+                continue
+            for lo in range(offs[c], offs[c + 1], max_rows):
+                mem = order[lo:min(offs[c + 1], lo + max_rows)]
+                d = sq[mem][:, None] + sq[cand][None, :] - 2.0 * (x[mem].float() @ xc.T)
+                d = torch.where(mem[:, None] == cand[None, :], float("inf"), d)
+                dv, di = torch.topk(d, kk, dim=1, largest=False)
+                out_i[mem, :kk] = torch.where(torch.isinf(dv), torch.full_like(di, -1), cand[di])
+                out_d[mem, :kk] = dv.clamp_min(0)
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out_i, out_d
+
+
+def medoid_of(x, chunk: int = 1 << 21) -> int:
+    """compute_medoid (graph.py:107-115) on the device: f64 mean, f64 distances."""
+    import torch
+    n = x.shape[0]
+    mean = torch.zeros(x.shape[1], dtype=torch.float64, device=x.device)
+    for lo in range(0, n, chunk):
+        mean += x[lo:lo + chunk].double().sum(0)
+    mean /= n
+    best_v, best_i = None, 0
+    for lo in range(0, n, chunk):
+        d = (x[lo:lo + chunk].double() - mean).square().sum(1)
+        v, i = torch.min(d, 0)
+        if best_v is None or float(v) < best_v:
+            best_v, best_i = float(v), lo + int(i)
+    return best_i
+
+
+def build_graph(base, degree_bound: int = 64, build_worklist: int = 200, sigma: float = 1.2,
+                seed: int = 0, candidates: int | None = None, exact_limit: int = 2_000_000,
+                device=None, log=None) -> GraphIndex:
+    """k-NN candidates (2R by default) -> RobustPrune(sigma) -> reverse edges.
+    Exact k-NN up to exact_limit points, partitioned (IVF) k-NN above."""
+    import time
+    import torch
+    dev = device if device is not None else torch_device()
     xn = np.asarray(base)
     n = xn.shape[0]
     R = int(degree_bound)
@@ -156,14 +265,81 @@ def build_graph(base, degree_bound: int = 64, build_worklist: int = 200, sigma: 
         raise ValueError("need at least 2 points to build a graph")
     x = torch.from_numpy(np.ascontiguousarray(xn, dtype=np.float32)).to(dev)
     K = min(n - 1, candidates or max(2 * R, min(build_worklist, 3 * R)))
-    ids, d = knn(x, K)
+    t0 = time.time()
+    if n <= exact_limit:
+        ids, d = knn(x, K)
+        medoid = compute_medoid(xn)
+    else:
+        ids, d = knn_ivf(x, K, seed=seed)
+        medoid = medoid_of(x)
+    t1 = time.time()
     ids, d = _sort_rows_by_dist(ids, d)
+    ids = torch.where(torch.isinf(d), torch.full_like(ids, -1), ids)
     adj, deg = robust_prune(x, ids, d, R, sigma)
+    del ids, d
+    t2 = time.time()
     adj, deg = add_reverse_edges(x, adj, deg, R, sigma)
-    medoid = compute_medoid(xn)
+    t3 = time.time()
+    if log:
+        log(f"[graph_build] n={n} knn {t1 - t0:.1f}s prune {t2 - t1:.1f}s reverse {t3 - t2:.1f}s")
     # the medoid must not be a dead end on a pathological input
-    adj_np = adj.cpu().numpy().astype(np.int32)
-    deg_np = deg.cpu().numpy().astype(np.int32)
+    adj_np = adj.to(torch.int32).cpu().numpy()
+    deg_np = deg.to(torch.int32).cpu().numpy()
     cols = np.arange(R)[None, :]
     adj_np[cols >= deg_np[:, None]] = -1
     return GraphIndex(adj_np, deg_np, medoid, R, validate=False)
+
+
+def refine_graph(x, adj, deg, visit_fn, R: int, sigma: float = 1.2, chunk: int = 1 << 20,
+                 max_cand: int = 192, log=None):
+    """One batch-synchronous Vamana pass (graph.py:251-344 semantics, all
+    points at once against the previous graph): for every point p the nodes
+    its greedy search expands (visit_fn(lo, hi) -> CSR offsets/ids of the
+    searches for points lo..hi-1) plus its current neighbours are the
+    candidates; RobustPrune(sigma) keeps R; reverse edges are added and
+    overflowing rows re-pruned.  adj/deg are torch tensors on x's device."""
+    import time
+    import torch
+    n = x.shape[0]
+    new_adj = torch.full((n, R), -1, dtype=torch.int64, device=x.device)
+    new_deg = torch.zeros(n, dtype=torch.int64, device=x.device)
+    t_search = t_prune = 0.0
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        t0 = time.time()
+        offs, flat = visit_fn(lo, hi)
+        t1 = time.time()
+        b = hi - lo
+        offs = torch.as_tensor(np.asarray(offs, np.int64), device=x.device)
+        flat = torch.as_tensor(np.asarray(flat, np.int64), device=x.device)
+        lens = offs[1:] - offs[:-1]
+        W = int(lens.max().item()) if b else 0
+        vis = torch.full((b, max(W, 1)), -1, dtype=torch.int64, device=x.device)
+        rows = torch.repeat_interleave(torch.arange(b, device=x.device), lens)
+        cols = torch.arange(flat.numel(), device=x.device) - offs[:-1][rows]
+        vis[rows, cols] = flat
+        cand = torch.cat([vis, adj[lo:hi].long()], 1)
+        self_ids = torch.arange(lo, hi, device=x.device)[:, None]
+        cand = torch.where(cand == self_ids, torch.full_like(cand, -1), cand)
+        # unique per row
+        cs, _ = torch.sort(cand, dim=1)
+        dup = torch.zeros_like(cs, dtype=torch.bool)
+        dup[:, 1:] = cs[:, 1:] == cs[:, :-1]
+        cand = torch.where(dup, torch.full_like(cs, -1), cs)
+        valid = cand >= 0
+        cd = torch.full(cand.shape, float("inf"), dtype=torch.float32, device=x.device)
+        rr = torch.arange(lo, hi, device=x.device)[:, None].expand_as(cand)
+        cd[valid] = _pair_sqdist(x, rr[valid], cand[valid])
+        cand, cd = _sort_rows_by_dist(cand, cd)
+        cand, cd = cand[:, :max_cand], cd[:, :max_cand]
+        cand = torch.where(torch.isinf(cd), torch.full_like(cand, -1), cand)
+        a, d = robust_prune(x, cand, cd, R, sigma)
+        new_adj[lo:hi] = a
+        new_deg[lo:hi] = d
+        t_search += t1 - t0
+        t_prune += time.time() - t1
+    t2 = time.time()
+    new_adj, new_deg = add_reverse_edges(x, new_adj, new_deg, R, sigma)
+    if log:
+        log(f"[graph_build] refine: search {t_search:.1f}s prune {t_prune:.1f}s reverse {time.time() - t2:.1f}s")
+    return new_adj, new_deg

@@ -27,9 +27,10 @@ def _subspace_views(x, sizes):
     return out  # zero-padded to a common width: padding adds 0 to every distance
 
 
-def train_codebook(base, m: int, iters: int = 25, seed: int = 0, sample: int = 262_144) -> PQCodebook:
+def train_codebook(base, m: int, iters: int = 25, seed: int = 0, sample: int = 262_144,
+                   device=None) -> PQCodebook:
     import torch
-    dev = torch_device()
+    dev = device if device is not None else torch_device()
     x = np.asarray(base)
     n, dim = x.shape
     sizes = subspace_split(dim, m)
@@ -54,10 +55,10 @@ def train_codebook(base, m: int, iters: int = 25, seed: int = 0, sample: int = 2
                       centroids=[np.ascontiguousarray(cents[s, :, :sz]) for s, sz in enumerate(sizes)])
 
 
-def encode(base, codebook: PQCodebook, chunk: int = 262_144) -> CompressedVectors:
+def encode(base, codebook: PQCodebook, chunk: int = 262_144, device=None) -> CompressedVectors:
     """Nearest centroid per subspace, exact f64 distances (lowest id on ties)."""
     import torch
-    dev = torch_device()
+    dev = device if device is not None else torch_device()
     x = np.asarray(base)
     out = np.empty((x.shape[0], codebook.m), np.uint8)
     cents = [torch.from_numpy(c.astype(np.float64)).to(dev) for c in codebook.centroids]

@@ -3,7 +3,7 @@
 # list + one full capture of the search kernel.  Usage (from the repo root):
 #   gpurun --timeout 3000 -- 'bash scripts/gpu_round.sh [CONFIG] [TAG]'
 set -u
-CFG=${1:-C2}
+CFG=${1:-C3}
 TAG=${2:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
@@ -14,6 +14,9 @@ tail -3 $OUT/pytest_gpu_$TAG.log
 timeout 1500 python bench.py --config $CFG > $OUT/bench_${CFG}_$TAG.json 2> $OUT/bench_${CFG}_$TAG.err; echo "bench rc=$?"
 cat $OUT/bench_${CFG}_$TAG.json
 T=$(python -c "import json,sys; print(json.load(open('$OUT/bench_${CFG}_$TAG.json'))['config']['t'])" 2>/dev/null || echo 32)
+timeout 600 python bench.py --config $CFG --t $T --phases --steps 2 --warmup 3 --no-cpu-baseline \
+  > $OUT/phases_${CFG}_$TAG.json 2> $OUT/phases_${CFG}_$TAG.err; echo "phases rc=$?"
+python -c "import json; print(json.load(open('$OUT/phases_${CFG}_$TAG.json'))['phase_cycles_per_iteration'])"
 timeout 900 python bench.py --config $CFG --impl reference --steps 2 --warmup 1 > $OUT/bench_ref_${CFG}_$TAG.json 2> $OUT/bench_ref_${CFG}_$TAG.err; echo "ref rc=$?"
 cat $OUT/bench_ref_${CFG}_$TAG.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
