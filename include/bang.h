@@ -54,6 +54,8 @@ typedef int32_t bang_status;
 #define BANG_PROFILE_PHASES 64 /* accumulate per-phase cycles (diagnostics, slower)  */
 #define BANG_DEBUG_GENERIC 128 /* use the generic search kernel even where a specialised one exists */
 #define BANG_WARP_PER_QUERY 256 /* smem-table ADC with one warp per query instead of one CTA */
+#define BANG_QUERY_POOL 512    /* lockstep query pool per CTA, CTA-shared codebook ADC        */
+#define BANG_NO_POOL 1024      /* never pick the query-pool kernel automatically               */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 

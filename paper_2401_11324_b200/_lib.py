@@ -34,6 +34,8 @@ CODEBOOK_SMEM = 32
 PROFILE_PHASES = 64
 DEBUG_GENERIC = 128
 WARP_PER_QUERY = 256
+QUERY_POOL = 512
+NO_POOL = 1024
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 
 _P = ctypes.c_void_p

@@ -18,6 +18,7 @@
 #include "bang_kernels.cuh"
 #include "bang_search_tab.cuh"
 #include "bang_search_cta.cuh"
+#include "bang_search_pool.cuh"
 
 using namespace bang;
 
@@ -126,6 +127,8 @@ struct Plan {
     int npl = 2, sub = 0, mv = 0;
     bool tab_kernel = false;  // search_tab_kernel (smem table + 16-byte code rows)
     bool cta_kernel = false;  // search_cta_kernel (one CTA per query, smem table)
+    bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
+    int pool_slots = 0, rr_ctas = 0;
     int nt = 0;               // threads per CTA of the CTA kernel
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
@@ -169,6 +172,60 @@ const void *pick_cta_kernel(int nt, int sub, int mv) {
     BANG_C(64, 0, 3) BANG_C(128, 0, 3) BANG_C(256, 0, 3)
 #undef BANG_C
     return nullptr;
+}
+
+template <int SUB, int MV, int RPAD>
+const void *pool_kernel_ptr() {
+    return reinterpret_cast<const void *>(&search_pool_kernel<SUB, MV, RPAD>);
+}
+
+const void *pick_pool_kernel(int sub, int mv, int rpad) {
+#define BANG_P(S, V, P) \
+    if (sub == S && mv == V && rpad == P) return pool_kernel_ptr<S, V, P>();
+    BANG_P(4, 2, 32) BANG_P(4, 2, 64) BANG_P(2, 3, 32) BANG_P(2, 3, 64)
+#undef BANG_P
+    return nullptr;
+}
+
+// Query-pool plan (search_pool_kernel): CTA-shared codebook + Q slots.
+bool plan_pool(bang_index *ix, int64_t nq, int t, int flags, Plan &pl) {
+    const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
+    const int sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
+    if (!sub || ix->R > 64 || (flags & (BANG_EXACT_DISTANCE | BANG_TABLE_GLOBAL | BANG_TABLE_SMEM |
+                                        BANG_CODEBOOK_SMEM | BANG_DEBUG_GENERIC | BANG_WARP_PER_QUERY)))
+        return false;
+    const int rpad = ix->R <= 32 ? 32 : 64;
+    int off = 0;
+    auto take = [&](int64_t bytes) { const int o = off; off += (int)align_up(bytes, 16); return o; };
+    pl.off_q = take(4LL * ix->dim);
+    pl.off_wl = take(8LL * t);
+    pl.off_nk = take(8LL * rpad);
+    pl.off_sk = take(8LL * rpad);
+    pl.off_fid = take(4LL * rpad);
+    pl.off_alive = take(rpad);
+    pl.off_acc = take(128);  // PoolCtl
+    pl.off_vis = take(t);
+    pl.off_sum = take(4LL * pl.sum_words);
+    pl.off_tab = off;
+    pl.per_warp = off;  // bytes per slot
+    pl.shared_bytes = (int)align_up((int64_t)256 * ix->dim * 4, 16);
+    const int q = (int)std::min<int64_t>(kPoolMaxSlots, (ix->max_smem - pl.shared_bytes) / pl.per_warp);
+    if (q < 8) return false;  // too few queries per SM to beat the table kernels
+    const void *kp = pick_pool_kernel(sub, mv, rpad);
+    if (!kp) return false;
+    pl.pool_kernel = true;
+    pl.variant = kAdcSmemCodebook;
+    pl.sub = sub;
+    pl.mv = mv;
+    pl.npl = rpad / 32;
+    pl.pool_slots = q;
+    pl.nt = kPoolThreads;
+    pl.warps = kPoolThreads / 32;
+    pl.smem = pl.shared_bytes + q * pl.per_warp;
+    pl.ctas = (int)std::min<int64_t>(ix->sm_count, std::max<int64_t>(1, ceil_div(nq, q)));
+    pl.slots = pl.ctas * q;
+    pl.rr_ctas = (int)std::min<int64_t>(4LL * ix->sm_count, std::max<int64_t>(1, ceil_div(nq, 8)));
+    return true;
 }
 
 const void *pick_kernel(int npl, int sub, int mv) {
@@ -228,6 +285,15 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.variant = kAdcSmemCodebook;
     } else {
         pl.variant = kAdcGlobalTable;
+    }
+    if ((flags & BANG_QUERY_POOL) && !(flags & BANG_NO_POOL)) {
+        if (plan_pool(ix, nq, t, flags, pl)) {
+            CU(cudaFuncSetAttribute(pick_pool_kernel(pl.sub, pl.mv, pl.npl * 32),
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+            return BANG_OK;
+        }
+        return fail(BANG_E_PARAM, "the query-pool kernel does not support this index/flags (m=%d, sub=%d, R=%d)",
+                    ix->m, ix->uniform_sub, ix->R);
     }
     pl.off_tab = pl.per_warp;
     if (pl.variant == kAdcSmemTable) pl.per_warp += (int)tab_bytes;
@@ -307,7 +373,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
                         float *d_dists, int32_t *d_iters, uint8_t *d_short, int32_t *d_log,
                         int64_t log_cap, const float *d_table, cudaStream_t st) {
     if (ix->bloom.reserve((size_t)pl.slots * pl.bloom_stride)) return BANG_E_OOM;
-    if (ix->rr.reserve((size_t)pl.slots * log_cap)) return BANG_E_OOM;
+    if (ix->rr.reserve((size_t)(pl.pool_kernel ? pl.rr_ctas * 8 : pl.slots) * log_cap)) return BANG_E_OOM;
     SearchParams p{};
     p.codes = ix->codes;
     p.centroids = ix->centroids;
@@ -360,9 +426,19 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_sum = pl.off_sum;
     p.sum_words = pl.sum_words;
     p.off_tab = pl.off_tab;
+    p.pool_slots = pl.pool_slots;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
+    if (pl.pool_kernel) {
+        void *pargs[] = {&p};
+        CU(cudaLaunchKernel(pick_pool_kernel(pl.sub, pl.mv, pl.npl * 32), dim3(pl.ctas), dim3(kPoolThreads), pargs,
+                            (size_t)pl.smem, st));
+        if (p.rerank)
+            rerank_log_kernel<<<pl.rr_ctas, 256, (size_t)8 * ix->dim * sizeof(float), st>>>(p);
+        CU(cudaGetLastError());
+        return BANG_OK;
+    }
     const void *kfn = pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);

@@ -69,6 +69,7 @@ struct SearchParams {
     int32_t smem_shared_bytes, per_warp_bytes;
     int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
+    int32_t pool_slots; // search_pool_kernel: query slots per CTA
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

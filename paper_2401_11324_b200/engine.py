@@ -318,7 +318,9 @@ class GraphSearcher(BaseEstimator):
                   # the smem table through the generic kernel (cross-check of the specialised one)
                   "smem-table-generic": _lib.TABLE_SMEM | _lib.DEBUG_GENERIC,
                   # the smem table with one warp (not one CTA) per query
-                  "smem-table-warp": _lib.TABLE_SMEM | _lib.WARP_PER_QUERY}
+                  "smem-table-warp": _lib.TABLE_SMEM | _lib.WARP_PER_QUERY,
+                  # lockstep query pool per CTA with the CTA-shared codebook
+                  "pool": _lib.QUERY_POOL}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):

@@ -302,9 +302,59 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
                     adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
                     k=10, t=t, bloom_entries=399_887, threads=8)
-    for variant in ("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table"):
+    variants = ["auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table"]
+    if m in (32, 48) and R <= 64:
+        variants.append("pool")
+    for variant in variants:
         res = s.set_adc_variant(variant).search(q)
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+
+
+@pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank,nq", [
+    (5, 20_000, 96, 64, 48, 32, np.float32, 1021, True, 500),     # collision-heavy Bloom: replay path
+    (6, 20_000, 128, 64, 32, 40, np.uint8, 4099, False, 300),     # no re-rank: wl[0:k] outputs
+    (7, 12_000, 128, 32, 32, 24, np.float32, 399_887, True, 700), # R=32 rows (one probe per thread)
+    (8, 12_000, 96, 48, 48, 100, np.float32, 399_887, True, 5),   # fewer queries than pool slots
+    (9, 12_000, 96, 64, 48, 16, np.float32, 251, True, 400),      # tiny filter: most rows collide
+])
+def test_pool_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank, nq):
+    """search_pool_kernel (lockstep query pool, CTA-shared codebook) against
+    the oracle: visit logs, iterations, ids, dists, short -- bit for bit."""
+    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, nq, dtype)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, rerank=rerank, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=10, t=t, bloom_entries=z, rerank=rerank, threads=8)
+    res = s.set_adc_variant("pool").search(q)
+    st = s.last_stats()
+    assert st["warps_per_cta"] == 24 and st["adc_variant"] == 0
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    assert st["iterations"] == int(res.iterations.sum())
+    if rerank:
+        assert st["rerank_cands"] == int(res.iterations.sum())
+
+
+def test_pool_kernel_overflow_retry_is_exact():
+    from paper_2401_11324_b200 import _lib
+    base, q, graph, cb, codes = _random_case(10, 10_000, 96, 64, 48, 200, np.float32)
+    t = 64
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887).set_adc_variant("pool")
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    _lib.check(_lib.lib().bang_index_set_log_capacity(s.index_.handle, 60))
+    res = s.search(q)
+    assert s.last_stats()["retries"] > 0
+    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=10, t=t, bloom_entries=399_887, threads=8)
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+
+
+def test_pool_kernel_rejects_unsupported_shapes():
+    g = gu.load("search_vamana_f32.npz")  # m=4: no 16-byte code rows
+    s = _searcher_from_golden(g).set_adc_variant("pool")
+    with pytest.raises(B.ParameterError):
+        s.search(g["queries"])
 
 
 def test_visit_log_overflow_retry_is_exact():
