@@ -139,7 +139,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
     ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
-    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool"))
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool", "smem-table-nofat"))
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -331,14 +331,15 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(args.config)
+            kname = _lib.KERNELS.get(s_last.get("kernel", 0), "?")
+            tr = json.load(f).get(f"{args.config}/{kname}")
             if tr and tr.get("t") == t_sel:
                 traffic = tr["dram_bytes_per_launch"]
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "bang::search_kernel", "kernel_ms": round(avg_kern_ms, 4),
+                "kernel": "bang::" + _lib.KERNELS.get(s_last.get("kernel", 0), "?"), "kernel_ms": round(avg_kern_ms, 4),
                 "algorithmic_bytes": s_last["algorithmic_bytes"],
                 "adc_bytes": s_last["adc_bytes"],
                 "adc_gbs": round(s_last["adc_bytes"] / (avg_kern_ms / 1000.0) / 1e9, 1)}
@@ -361,12 +362,19 @@ def main():
            "roofline": roofline, "cpu_baseline": cpu,
            "clocks": clk.summary(),
            "search_stats": {kk: s_last[kk] for kk in ("iterations", "probes", "fresh", "rerank_cands", "slots",
-                                                      "warps_per_cta", "ctas", "adc_variant", "retries")},
+                                                      "warps_per_cta", "ctas", "adc_variant", "retries",
+                                                      "kernel")},
            "step_ms": [round(x, 4) for x in step_ms]}
     if args.phases:
         pc = s_last["phase_cycles"]
         it = max(1, s_last["iterations"])
-        if s_last["slots"] == s_last["ctas"]:  # search_cta_kernel: thread 0's cycles
+        if s_last["warps_per_cta"] == 24 and s_last["adc_variant"] == 0:  # search_pool_kernel
+            names = ["issue_expand", "bloom_wait_t0", "bloom_barrier", "zeroing", "atomics_adc_t0",
+                     "adc_barrier", "replay_owner", "loop_barrier"]
+            out["phase_cycles_per_pool_iteration"] = {
+                nm: round(pc[i] / max(1, s_last["iterations"] / max(1, s_last["slots"])) / max(1, s_last["ctas"]), 1)
+                for i, nm in enumerate(names)}
+        elif s_last["slots"] == s_last["ctas"]:  # search_cta_kernel: thread 0's cycles
             names = ["bloom_load", "zero_sync", "adc_reduce", "coll_sync", "winner_prefetch", "sort", "merge"]
             out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
             out["phase_cycles_per_iteration"]["epilogue_per_query"] = round(pc[7] / max(1, nq), 1)

@@ -56,6 +56,7 @@ typedef int32_t bang_status;
 #define BANG_WARP_PER_QUERY 256 /* smem-table ADC with one warp per query instead of one CTA */
 #define BANG_QUERY_POOL 512    /* lockstep query pool per CTA, CTA-shared codebook ADC        */
 #define BANG_NO_POOL 1024      /* never pick the query-pool kernel automatically               */
+#define BANG_NO_FAT 2048       /* do not use the fat-row (inline neighbour codes) CTA kernel  */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 
@@ -80,6 +81,9 @@ typedef struct bang_search_stats {
                                  summed over warps: 0 adjacency wait, 1 expand,
                                  2 Bloom issue, 3 ADC, 4 Bloom resolve, 5 sort +
                                  eager + prefetch, 6 merge + converge, 7 unused */
+    int32_t kernel;           /* 0 warp/query, 1 warp/query smem table, 2 CTA/query,
+                                 3 CTA/query over fat rows, 4 query pool         */
+    int32_t reserved;
 } bang_search_stats;
 
 /* ---------------------------------------------------------------- errors */

@@ -36,7 +36,10 @@ DEBUG_GENERIC = 128
 WARP_PER_QUERY = 256
 QUERY_POOL = 512
 NO_POOL = 1024
+NO_FAT = 2048
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
+KERNELS = {0: "search_kernel", 1: "search_tab_kernel", 2: "search_cta_kernel", 3: "search_fat_kernel",
+           4: "search_pool_kernel"}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -53,6 +56,7 @@ class SearchStats(ctypes.Structure):
         ("kernel_ms", ctypes.c_float), ("table_ms", ctypes.c_float),
         ("algorithmic_bytes", ctypes.c_int64), ("adc_bytes", ctypes.c_int64),
         ("phase_cycles", ctypes.c_int64 * 8),
+        ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self):

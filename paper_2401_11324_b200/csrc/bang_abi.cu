@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "bang_search_tab.cuh"
 #include "bang_search_cta.cuh"
 #include "bang_search_pool.cuh"
+#include "bang_search_fat.cuh"
 
 using namespace bang;
 
@@ -92,6 +94,10 @@ struct bang_index {
     int32_t *adj = nullptr, *deg = nullptr;
     void *vectors = nullptr;
     bool host_graph = false;
+    // fat rows (bang_search_fat.cuh): ids + inline neighbour codes, HBM only
+    uint8_t *fat = nullptr;
+    int64_t fat_stride = 0;
+    int32_t fat_code_off = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int sm_count = 148;
@@ -128,6 +134,8 @@ struct Plan {
     bool tab_kernel = false;  // search_tab_kernel (smem table + 16-byte code rows)
     bool cta_kernel = false;  // search_cta_kernel (one CTA per query, smem table)
     bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
+    bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
+    int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
     int nt = 0;               // threads per CTA of the CTA kernel
     int warps = 32, ctas = 148, slots = 0;
@@ -174,6 +182,19 @@ const void *pick_cta_kernel(int nt, int sub, int mv) {
     return nullptr;
 }
 
+template <int NT, int SUB, int MV>
+const void *fat_kernel_ptr() {
+    return reinterpret_cast<const void *>(&search_fat_kernel<NT, SUB, MV, MV == 3 ? 4 : 6>);
+}
+
+const void *pick_fat_kernel(int nt, int sub, int mv) {
+#define BANG_F(N, S, V) \
+    if (nt == N && sub == S && mv == V) return fat_kernel_ptr<N, S, V>();
+    BANG_F(64, 4, 2) BANG_F(128, 4, 2) BANG_F(64, 2, 3) BANG_F(128, 2, 3)
+#undef BANG_F
+    return nullptr;
+}
+
 template <int SUB, int MV, int RPAD>
 const void *pool_kernel_ptr() {
     return reinterpret_cast<const void *>(&search_pool_kernel<SUB, MV, RPAD>);
@@ -208,7 +229,7 @@ bool plan_pool(bang_index *ix, int64_t nq, int t, int flags, Plan &pl) {
     pl.off_sum = take(4LL * pl.sum_words);
     pl.off_tab = off;
     pl.per_warp = off;  // bytes per slot
-    pl.shared_bytes = (int)align_up((int64_t)256 * ix->dim * 4, 16);
+    pl.shared_bytes = (int)align_up((int64_t)256 * ix->dim * 4, 16) + (int)sizeof(PoolCta);
     const int q = (int)std::min<int64_t>(kPoolMaxSlots, (ix->max_smem - pl.shared_bytes) / pl.per_warp);
     if (q < 8) return false;  // too few queries per SM to beat the table kernels
     const void *kp = pick_pool_kernel(sub, mv, rpad);
@@ -328,12 +349,17 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_vis = take(t);
         pl.off_sum = take(4LL * pl.sum_words);
         pl.off_tab = take(tab_bytes);
+        pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
+        if (pl.fat_kernel) {
+            pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
+            pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
+        }
         pl.per_warp = off;  // bytes per CTA
         pl.shared_bytes = 0;
         pl.warps = pl.nt / 32;
         pl.smem = pl.per_warp;
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
-        const void *kc = pick_cta_kernel(pl.nt, pl.sub, pl.mv);
+        const void *kc = pl.fat_kernel ? pick_fat_kernel(pl.nt, pl.sub, pl.mv) : pick_cta_kernel(pl.nt, pl.sub, pl.mv);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
         int per_sm = 0;
@@ -427,6 +453,10 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.sum_words = pl.sum_words;
     p.off_tab = pl.off_tab;
     p.pool_slots = pl.pool_slots;
+    p.fat = ix->fat;
+    p.fat_stride = ix->fat_stride;
+    p.fat_code_off = ix->fat_code_off;
+    p.off_dup = pl.off_dup;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -439,7 +469,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
         CU(cudaGetLastError());
         return BANG_OK;
     }
-    const void *kfn = pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
+    const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
@@ -506,6 +537,7 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
     ix->stats.warps_per_cta = pl.warps;
     ix->stats.ctas = pl.ctas;
     ix->stats.adc_variant = pl.variant;
+    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
     ix->last_nq = nq;
     ix->last_log_cap = cap;
     ix->last_has_table = d_table != nullptr;
@@ -533,8 +565,10 @@ bang_status collect(bang_index *ix, unsigned long long *ctr) {
     // adjacency rows + degree, two Bloom words
     // read per probe and written per admission, code rows of the admitted,
     // re-rank vectors, queries in, results + visit logs out.
+    // (fat rows: the code rows of every expanded neighbour arrive with the ids)
+    const int64_t code_rows = S.kernel == 3 ? S.probes : S.fresh;
     S.algorithmic_bytes = S.iterations * 8 + S.probes * 4 + S.probes * 8 + S.fresh * 8 +
-                          S.fresh * ix->m + S.rerank_cands * ix->dim * elem +
+                          code_rows * ix->m + S.rerank_cands * ix->dim * elem +
                           S.queries * (ix->dim * 4 + 16);
     S.adc_bytes = S.fresh * (ix->m + 12);
     for (int i = 0; i < 8; ++i) S.phase_cycles[i] = (int64_t)ctr[kCtrPhase0 + i];
@@ -649,6 +683,23 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
         CUX(cudaMemcpy(ix->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->deg, degrees, deg_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->vectors, vectors, vec_bytes, cudaMemcpyHostToDevice));
+        // fat rows for the CTA-per-query kernel: ids + the neighbours' code rows
+        // inline (one coalesced read per hop); optional -- skipped when HBM is short
+        const char *nofat = getenv("BANG_NO_FAT");
+        if (m > 0 && m % 16 == 0 && m / 16 <= 3 && !(nofat && *nofat && *nofat != '0')) {
+            ix->fat_code_off = (int32_t)align_up(4LL * R, 16);
+            ix->fat_stride = align_up(ix->fat_code_off + (int64_t)R * m, 16);
+            if (cudaMalloc(&ix->fat, (size_t)n * ix->fat_stride) == cudaSuccess) {
+                const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)ix->sm_count * 16);
+                build_fat_rows_kernel<<<(unsigned)blocks, 256, 0, ix->stream>>>(
+                    ix->adj, ix->deg, ix->codes, n, R, m, ix->fat_code_off, ix->fat_stride, ix->fat);
+                CUX(cudaGetLastError());
+                CUX(cudaStreamSynchronize(ix->stream));
+            } else {
+                cudaGetLastError();
+                ix->fat = nullptr;
+            }
+        }
     } else {
         return cleanup_fail(fail(BANG_E_PARAM, "unknown graph placement %d", graph_placement));
     }
@@ -662,6 +713,7 @@ void bang_index_destroy(bang_index *ix) {
     cudaSetDevice(ix->device);
     if (ix->stream) cudaStreamSynchronize(ix->stream);
     cudaFree(ix->codes);
+    cudaFree(ix->fat);
     cudaFree(ix->centroids);
     cudaFree(ix->d_sub_off);
     cudaFree(ix->d_sub_size);

@@ -70,6 +70,10 @@ struct SearchParams {
     int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
     int32_t pool_slots; // search_pool_kernel: query slots per CTA
+    // search_fat_kernel: rows [ids R x i32 | pad | codes R x m] (bang_search_fat.cuh)
+    const uint8_t *fat;
+    int64_t fat_stride;
+    int32_t fat_code_off, off_dup;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

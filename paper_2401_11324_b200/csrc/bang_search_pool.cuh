@@ -50,6 +50,14 @@ struct PoolCtl {
 };
 static_assert(sizeof(PoolCtl) <= 128, "PoolCtl must fit its 128-byte slot");
 
+// CTA-wide scratch after the codebook (phase profiler: thread 0's cycles)
+struct PoolCta {
+    unsigned long long ph[8];
+    long long t_ph;
+    int pad[14];
+};
+static_assert(sizeof(PoolCta) == 128, "PoolCta is 128 bytes");
+
 template <int SUB, int MV, int RPAD>
 __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const SearchParams p) {
     constexpr int NT = kPoolThreads;
@@ -68,6 +76,17 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
         const float4 *src = reinterpret_cast<const float4 *>(p.centroids);
         float4 *dst = reinterpret_cast<float4 *>(s_cb);
         for (int i = tid; i < n4; i += NT) dst[i] = __ldg(src + i);
+    }
+    PoolCta *s_cta = reinterpret_cast<PoolCta *>(smem + p.smem_shared_bytes - sizeof(PoolCta));
+    if (tid == 0) {
+        for (int i = 0; i < 8; ++i) s_cta->ph[i] = 0;
+        s_cta->t_ph = clock64();
+    }
+#define BANG_POOL_PHASE(i)                                           \
+    if (p.profile && tid == 0) {                                     \
+        const long long now_ = clock64();                            \
+        s_cta->ph[i] += (unsigned long long)(now_ - s_cta->t_ph);    \
+        s_cta->t_ph = now_;                                          \
     }
     auto sbase = [&](int s) { return smem + p.smem_shared_bytes + (size_t)s * p.per_warp_bytes; };
     auto S_q = [&](int s) { return reinterpret_cast<float *>(sbase(s) + p.off_q); };
@@ -167,6 +186,7 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
 
     for (;;) {
         if (!__syncthreads_or(warp < Q && lane == 0 && S_ctl(warp)->active)) break;
+        BANG_POOL_PHASE(7)  // loop-top barrier (waits for the slowest owner warp)
 
         // ================= phase 1: probes (pre-state) + code rows in flight
         uint32_t ps1[IPT], ps2[IPT], w1[IPT], w2[IPT], o1[IPT], o2[IPT], nid[IPT];
@@ -223,10 +243,14 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
                 st_probes += c->deg;
             }
         }
+        BANG_POOL_PHASE(0)  // issue + owner expand
 #pragma unroll
         for (int k = 0; k < IPT; ++k)
             fresh[k] = valid[k] && !(((w1[k] >> (ps1[k] & 31)) & 1u) && ((w2[k] >> (ps2[k] & 31)) & 1u));
+        if (p.profile) asm volatile("" ::"r"((int)fresh[0]));
+        BANG_POOL_PHASE(1)  // Bloom word loads landed (thread 0)
         __syncthreads();  // every summary read and pre-state load precedes the writes below
+        BANG_POOL_PHASE(2)  // barrier: slowest load in the CTA
 
         // ================= phase 2: words first written by this query
 #pragma unroll
@@ -246,6 +270,7 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
             }
         }
         __syncthreads();  // zeroing stores (any thread) before any atomic
+        BANG_POOL_PHASE(3)
 
         // ================= phase 3: atomics in flight, ADC from the codebook
 #pragma unroll
@@ -295,7 +320,10 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
                 }
             }
         }
-        if (__syncthreads_or(coll)) {
+        BANG_POOL_PHASE(4)  // atomics + ADC (thread 0's items)
+        const int any_coll = __syncthreads_or(coll);
+        BANG_POOL_PHASE(5)  // barrier: slowest ADC in the CTA
+        if (any_coll) {
             // ============= phase 4 (rare): in-row slot sharing, exact replay
             // probe records of the rows with a collision -> smem scratch
 #pragma unroll
@@ -468,7 +496,11 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
                 }
             }
         }
+        BANG_POOL_PHASE(6)  // rare replay + owner phase (slot 0)
     }
+#undef BANG_POOL_PHASE
+    if (p.profile && tid == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(p.counters + kCtrPhase0 + i, s_cta->ph[i]);
     if (lane == 0) {
         atomicAdd(p.counters + kCtrIterations, st_iters);
         atomicAdd(p.counters + kCtrProbes, st_probes);

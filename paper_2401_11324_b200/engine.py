@@ -320,7 +320,9 @@ class GraphSearcher(BaseEstimator):
                   # the smem table with one warp (not one CTA) per query
                   "smem-table-warp": _lib.TABLE_SMEM | _lib.WARP_PER_QUERY,
                   # lockstep query pool per CTA with the CTA-shared codebook
-                  "pool": _lib.QUERY_POOL}
+                  "pool": _lib.QUERY_POOL,
+                  # CTA per query without the fat-row layout (ids and codes read separately)
+                  "smem-table-nofat": _lib.TABLE_SMEM | _lib.NO_FAT}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):

@@ -302,9 +302,12 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
                     adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
                     k=10, t=t, bloom_entries=399_887, threads=8)
-    variants = ["auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table"]
+    variants = ["auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table",
+                "smem-table-nofat"]
     if m in (32, 48) and R <= 64:
         variants.append("pool")
+        s.set_adc_variant("auto").search(q[:4])
+        assert s.last_stats()["kernel"] == 3  # fat rows are the default CTA path in HBM
     for variant in variants:
         res = s.set_adc_variant(variant).search(q)
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
@@ -313,9 +316,9 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank,nq", [
     (5, 20_000, 96, 64, 48, 32, np.float32, 1021, True, 500),     # collision-heavy Bloom: replay path
     (6, 20_000, 128, 64, 32, 40, np.uint8, 4099, False, 300),     # no re-rank: wl[0:k] outputs
-    (7, 12_000, 128, 32, 32, 24, np.float32, 399_887, True, 700), # R=32 rows (one probe per thread)
-    (8, 12_000, 96, 48, 48, 100, np.float32, 399_887, True, 5),   # fewer queries than pool slots
-    (9, 12_000, 96, 64, 48, 16, np.float32, 251, True, 400),      # tiny filter: most rows collide
+    (7, 16_000, 128, 32, 32, 24, np.float32, 399_887, True, 700), # R=32 rows (one probe per thread)
+    (8, 16_000, 96, 48, 48, 100, np.float32, 399_887, True, 5),   # fewer queries than pool slots
+    (9, 16_000, 96, 64, 48, 16, np.float32, 251, True, 400),      # tiny filter: most rows collide
 ])
 def test_pool_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank, nq):
     """search_pool_kernel (lockstep query pool, CTA-shared codebook) against
@@ -333,6 +336,25 @@ def test_pool_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank, nq):
     assert st["iterations"] == int(res.iterations.sum())
     if rerank:
         assert st["rerank_cands"] == int(res.iterations.sum())
+
+
+@pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank", [
+    (11, 16_000, 96, 64, 48, 40, np.float32, 1021, True),    # collision-heavy: smem replay path
+    (12, 16_000, 128, 64, 32, 32, np.uint8, 251, False),     # tiny filter, no re-rank
+    (13, 16_000, 128, 40, 32, 64, np.float32, 399_887, True),  # R=40: padded slots, uneven degrees
+])
+def test_fat_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank):
+    """search_fat_kernel (fat rows, speculative ADC, smem slot-sharing table,
+    fire-and-forget Bloom sets) against the oracle, bit for bit."""
+    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 400, dtype)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, rerank=rerank, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=10, t=t, bloom_entries=z, rerank=rerank, threads=8)
+    res = s.search(q)
+    assert s.last_stats()["kernel"] == 3
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
 def test_pool_kernel_overflow_retry_is_exact():
