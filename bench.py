@@ -139,7 +139,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
     ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
-    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool", "smem-table-nofat"))
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool", "smem-table-nofat", "fat"))
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -183,8 +183,10 @@ def main():
     meta = art["meta"]
     searcher = GraphSearcher(k=k, t=max(T_SWEEP), mode="in_memory", bloom_entries=args.bloom,
                              batch_size=nq)
+    if args.variant == "fat":
+        os.environ["BANG_FAT_ROWS"] = "1"  # search_fat_kernel needs the fat rows built at load
     searcher.fit(art["base"], graph=art["graph"], codebook=art["codebook"], codes=art["codes"])
-    searcher.set_adc_variant(args.variant)
+    searcher.set_adc_variant("auto" if args.variant == "fat" else args.variant)
 
     # ---- worklist size at recall >= target (the metric's operating point)
     sweep = []
@@ -240,7 +242,7 @@ def main():
         return
 
     # ---- device-resident timing (value)
-    flags = _lib.RERANK | searcher._ADC_FLAGS[args.variant]
+    flags = _lib.RERANK | searcher._ADC_FLAGS["auto" if args.variant == "fat" else args.variant]
     if args.phases:
         flags |= _lib.PROFILE_PHASES
     dev = torch.device("cuda", local)

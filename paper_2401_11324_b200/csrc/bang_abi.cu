@@ -683,10 +683,11 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
         CUX(cudaMemcpy(ix->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->deg, degrees, deg_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->vectors, vectors, vec_bytes, cudaMemcpyHostToDevice));
-        // fat rows for the CTA-per-query kernel: ids + the neighbours' code rows
-        // inline (one coalesced read per hop); optional -- skipped when HBM is short
-        const char *nofat = getenv("BANG_NO_FAT");
-        if (m > 0 && m % 16 == 0 && m / 16 <= 3 && !(nofat && *nofat && *nofat != '0')) {
+        // fat rows for search_fat_kernel: ids + the neighbours' code rows inline
+        // (one coalesced read per hop).  Opt-in (BANG_FAT_ROWS=1): measured
+        // slower than separate code rows at C2/C3 (profiles/r01/fat_rows.txt)
+        const char *fatenv = getenv("BANG_FAT_ROWS");
+        if (m > 0 && m % 16 == 0 && m / 16 <= 3 && fatenv && *fatenv == '1') {
             ix->fat_code_off = (int32_t)align_up(4LL * R, 16);
             ix->fat_stride = align_up(ix->fat_code_off + (int64_t)R * m, 16);
             if (cudaMalloc(&ix->fat, (size_t)n * ix->fat_stride) == cudaSuccess) {
