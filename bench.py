@@ -125,6 +125,59 @@ def cpu_oracle_qps(art, t, k, bloom, budget_s=12.0, max_q=None):
                        f"threads (OpenMP over queries)"), res
 
 
+def adc_pairs_roofline(searcher, art, queries, res, dev, stream, flush, peak, peak_kind, reps=3):
+    """Times kernel 3 (adc_pairs_kernel) over the pairs of the benchmark
+    search: for each query, the rows of every node it expanded (its Bloom
+    probes), in visit order.  Achieved = pairs x (m + 12) B / kernel time."""
+    import torch
+    from paper_2401_11324_b200 import _lib
+    g = art["graph"]
+    offs, flat = res.visit_logs.csr()
+    m = art["codebook"].m
+    adj = torch.from_numpy(np.ascontiguousarray(g.adjacency)).to(dev)
+    deg = torch.from_numpy(np.ascontiguousarray(g.degrees)).to(dev).long()
+    v = torch.from_numpy(np.asarray(flat, np.int64)).to(dev)
+    rows = adj[v]                                   # (visits, R)
+    mask = torch.arange(g.adjacency.shape[1], device=dev)[None, :] < deg[v][:, None]
+    ids = rows[mask].contiguous()                   # probes in visit order
+    per_visit = mask.sum(1)
+    qo = torch.from_numpy(np.asarray(offs, np.int64)).to(dev)
+    csum = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev), torch.cumsum(per_visit, 0)])
+    pair_off = csum[qo].contiguous()
+    del adj, rows, mask
+    dq = torch.from_numpy(np.ascontiguousarray(queries, np.float32)).to(dev)
+    keys = torch.empty(ids.numel(), dtype=torch.int64, device=dev)
+    L = _lib.lib()
+    h = searcher.index_.handle
+    nq = dq.shape[0]
+
+    def launch():
+        _lib.check(L.bang_adc_pairs_device(h, _lib.ptr(dq), nq, _lib.ptr(pair_off), _lib.ptr(ids),
+                                           _lib.ptr(keys), _lib.stream_ptr(stream)), "bang_adc_pairs_device")
+
+    launch()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = float(np.mean(ms))
+    pairs = int(ids.numel())
+    algo = pairs * (m + 12) + nq * (4 * queries.shape[1])
+    ach = algo / (t / 1000.0) / 1e9
+    return {"kernel": "bang::adc_pairs_kernel", "pairs": pairs, "queries": int(nq), "ms": round(t, 4),
+            "bytes_per_pair": m + 12, "algorithmic_bytes": algo, "achieved": round(ach, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(ach / peak, 4), "peak_kind": peak_kind,
+            "pairs_source": "every (query, neighbour) probe of the benchmark search, grouped by query "
+                            "(the rows of each query's visit log); table built in smem per query",
+            "l2": "flushed before each timed launch"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -346,6 +399,11 @@ def main():
                 "adc_bytes": s_last["adc_bytes"],
                 "adc_gbs": round(s_last["adc_bytes"] / (avg_kern_ms / 1000.0) / 1e9, 1)}
 
+    # ---- kernel 3 on its own (north_star "ADC kernel HBM GB/s vs peak",
+    # SURVEY.md 8(d)): every (query, neighbour) probe of this benchmark's
+    # searches, grouped by query, through bang_adc_pairs_device
+    adc_k = adc_pairs_roofline(searcher, art, shard["queries"], res, dev, stream, flush, peak, peak_kind, warm)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu, _ = cpu_oracle_qps(art, t_sel, k, args.bloom)
@@ -361,7 +419,7 @@ def main():
            "e2e": {"value": round(e2e_value, 1), "unit": "queries/s", "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": round(1000 * float(e2e_tot.item()) / steps, 3)},
            "gpu_launches": 2 * steps + (1 if s_last["adc_variant"] == 1 else 0) * steps,
-           "roofline": roofline, "cpu_baseline": cpu,
+           "roofline": roofline, "adc_kernel": adc_k, "cpu_baseline": cpu,
            "clocks": clk.summary(),
            "search_stats": {kk: s_last[kk] for kk in ("iterations", "probes", "fresh", "rerank_cands", "slots",
                                                       "warps_per_cta", "ctas", "adc_variant", "retries",

@@ -183,6 +183,15 @@ bang_status bang_adc_device(const float *d_table, int32_t m, const uint8_t *d_co
                             const int64_t *d_qrows, const uint32_t *d_ids, int64_t n,
                             float *d_dists, uint64_t *d_keys, void *stream);
 
+/* Kernel 3 over query-grouped pairs: one CTA per query builds
+ * its table in shared memory (kernel 1 fused), then keys[i] = pack(ADC(q, ids[i]),
+ * ids[i]) for i in [off[q], off[q+1]).  d_queries (nq, dim) f32; d_off (nq+1)
+ * int64 non-decreasing; d_keys (off[nq]) u64.  Same arithmetic as
+ * bang_adc_device on kernel 1's table (engine.py:99-105, pq.py:284-296). */
+bang_status bang_adc_pairs_device(bang_index *index, const float *d_queries, int64_t nq,
+                                  const int64_t *d_off, const uint32_t *d_ids, uint64_t *d_keys,
+                                  void *stream);
+
 /* Kernel 4a -- merge_sort_rows (kernels.py:94-109): ascending rows, in place. */
 bang_status bang_sort_rows_device(uint64_t *d_keys, int64_t rows, int32_t width, void *stream);
 /* Kernel 4b -- merge_rows (kernels.py:68-87): out (rows, wa+wb), a first on ties;

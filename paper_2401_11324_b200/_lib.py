@@ -84,6 +84,7 @@ _SIGS = {
     "bang_pq_table_device": (_I32, [_P, _P, _I32, _I32, _P, _I64, _P, _P]),
     "bang_bloom_filter_device": (_I32, [_P, _I64, _I64, _P, _P, _P, _P]),
     "bang_adc_device": (_I32, [_P, _I32, _P, _P, _P, _I64, _P, _P, _P]),
+    "bang_adc_pairs_device": (_I32, [_P, _P, _I64, _P, _P, _P, _P]),
     "bang_sort_rows_device": (_I32, [_P, _I64, _I32, _P]),
     "bang_merge_rows_device": (_I32, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
     "bang_worklist_update_device": (_I32, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),

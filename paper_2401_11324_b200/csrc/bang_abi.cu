@@ -979,6 +979,34 @@ bang_status bang_adc_device(const float *d_table, int32_t m, const uint8_t *d_co
     return BANG_OK;
 }
 
+bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_t nq, const int64_t *d_off,
+                                  const uint32_t *d_ids, uint64_t *d_keys, void *stream) {
+    if (!ix) return fail(BANG_E_STATE, "null index");
+    if (ix->m < 1) return fail(BANG_E_PARAM, "index has no PQ codes");
+    if (nq < 0) return fail(BANG_E_PARAM, "nq must be >= 0");
+    if (nq == 0) return BANG_OK;
+    CU(cudaSetDevice(ix->device));
+    cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : ix->stream;
+    const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
+    const int sub = ix->uniform_sub;
+    const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + ix->dim);
+    if (smem > (size_t)ix->max_smem) return fail(BANG_E_PARAM, "table of m=%d does not fit in shared memory", ix->m);
+    auto launch = [&](const void *fn) -> bang_status {
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+        const int64_t grid = std::min<int64_t>(nq, (int64_t)ix->sm_count * std::max(1, per_sm));
+        int m = ix->m, dim = ix->dim;
+        void *args[] = {&ix->centroids, &ix->d_sub_off, &ix->d_sub_size, &m, &dim, &d_queries, &nq,
+                        &d_off, &d_ids, &ix->codes, &d_keys};
+        CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st));
+        return BANG_OK;
+    };
+    if (sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<4, 2>));
+    if (sub == 2 && mv == 3) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<2, 3>));
+    return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<0, 0>));
+}
+
 bang_status bang_sort_rows_device(uint64_t *d_keys, int64_t rows, int32_t width, void *stream) {
     if (width < 0 || width > 6144) return fail(BANG_E_PARAM, "row width %d outside [0, 6144]", width);
     if (rows == 0 || width == 0) return BANG_OK;

@@ -790,3 +790,78 @@ __global__ void exact_dists_kernel(const void *points, int dtype, int dim,
 }
 
 }  // namespace bang
+
+namespace bang {
+// -------------------------------------------------------------------------
+// Kernel 3 over a query-grouped pair list (north_star kernel 3; SURVEY.md
+// 8(d) "a standalone ADC launch over all (query, neighbour) pairs"): one CTA
+// per query builds the query's table in shared memory (kernel 1, pq.py:284-296
+// op order), then every pair of that query gathers its PQ code row with
+// 16-byte loads and sums the table entries sequentially in f32
+// (engine.py:99-105).  keys[i] = f32bits << 32 | ids[i].  Pairs of query q are
+// ids[off[q], off[q+1]).  SUB/MV > 0: uniform subspaces of width SUB and
+// m = 16*MV (vector path); 0: generic.
+// -------------------------------------------------------------------------
+template <int SUB, int MV>
+__global__ void __launch_bounds__(256) adc_pairs_kernel(const float *__restrict__ centroids,
+                                                        const int32_t *__restrict__ sub_off,
+                                                        const int32_t *__restrict__ sub_size, int m,
+                                                        int dim, const float *__restrict__ queries,
+                                                        int64_t nq, const int64_t *__restrict__ off,
+                                                        const uint32_t *__restrict__ ids,
+                                                        const uint8_t *__restrict__ codes,
+                                                        uint64_t *__restrict__ keys) {
+    extern __shared__ __align__(16) float s_tab[];  // m*256 table, then the query
+    float *s_q = s_tab + (size_t)m * 256;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        for (int i = tid; i < dim; i += nt) s_q[i] = __ldg(queries + q * dim + i);
+        __syncthreads();
+        for (int idx = tid; idx < m * 256; idx += nt) {
+            const int s = idx >> 8, c = idx & 255;
+            float e;
+            if constexpr (SUB == 4) {
+                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                                 __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
+            } else if constexpr (SUB == 2) {
+                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                                 __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
+            } else {
+                const int o = __ldg(sub_off + s), sz = __ldg(sub_size + s);
+                e = table_entry(s_q + o, centroids + (int64_t)o * 256 + c * sz, sz);
+            }
+            s_tab[idx] = e;
+        }
+        __syncthreads();
+        const int64_t lo = off[q], hi = off[q + 1];
+        if constexpr (MV > 0) {
+            // two pairs per thread per step: both code rows in flight together
+            for (int64_t i = lo + tid; i < hi; i += 2 * nt) {
+                const int64_t i1 = i + nt;
+                const bool has1 = i1 < hi;
+                const uint32_t n0 = __ldg(ids + i), n1 = has1 ? __ldg(ids + i1) : n0;
+                uint4 c0[MV], c1[MV];
+#pragma unroll
+                for (int v = 0; v < MV; ++v) {
+                    c0[v] = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)n0 * (16 * MV)) + v);
+                    c1[v] = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)n1 * (16 * MV)) + v);
+                }
+                float a0 = 0.0f, a1 = 0.0f;
+#pragma unroll
+                for (int v = 0; v < MV; ++v) {
+                    a0 = adc_tab_stage16(a0, s_tab, 16 * v, c0[v]);
+                    a1 = adc_tab_stage16(a1, s_tab, 16 * v, c1[v]);
+                }
+                keys[i] = pack_key(a0, n0);
+                if (has1) keys[i1] = pack_key(a1, n1);
+            }
+        } else {
+            for (int64_t i = lo + tid; i < hi; i += nt) {
+                const uint32_t node = __ldg(ids + i);
+                keys[i] = pack_key(adc_table<0>(s_tab, m, codes + (int64_t)node * m), node);
+            }
+        }
+        __syncthreads();
+    }
+}
+}  // namespace bang

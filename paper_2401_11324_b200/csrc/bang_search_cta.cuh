@@ -134,35 +134,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
         uint32_t id = j < R ? (uint32_t)p.adj[(int64_t)u * R + j] : 0u;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
-        // Next-row issue: this half's code bytes, Bloom slot, summary bit and
-        // pre-state word.  For every row but the medoid's this runs during the
-        // previous iteration's merge, so the loads land while it merges.
-        uint32_t cw[MHW], ps = 0, word = 0;
-        bool init = true;
-        auto issue_row = [&](int dg) {
-            ps = 0;
-            word = 0;
-            init = true;
-            if (j < dg) {
-                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * M) + h * MHW;
-                if constexpr (MHW == 4) {
-                    const uint4 v = __ldcg(reinterpret_cast<const uint4 *>(row));
-                    cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
-                } else {
-#pragma unroll
-                    for (int q = 0; q < MHW; q += 2) {
-                        const uint2 v = __ldcg(reinterpret_cast<const uint2 *>(row + q));
-                        cw[q] = v.x;
-                        cw[q + 1] = v.y;
-                    }
-                }
-                ps = mod_z(fnv1a(id, hseed), p.geom);
-                init = sum_get(s_sum, ps >> 5);
-                if (init) word = __ldcg(bits + (ps >> 5));
-            }
-        };
-        __syncthreads();  // medoid bits + summary visible before the first issue
-        issue_row(deg);
+        __syncthreads();
 
         for (;;) {
             if (p.profile && tid == 0) s_m->t_ph = clock64();
@@ -184,9 +156,32 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             ++iters;
             st_probes += deg;
             const bool valid = j < deg;
-            // ---- kernel 2: Bloom test of this half's slot (pre-state; loads issued earlier)
+            // ---- this half's code bytes, in flight with the Bloom word
+            uint32_t cw[MHW];
+            if (valid) {
+                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * M) + h * MHW;
+                if constexpr (MHW == 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row));
+                    cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < MHW; q += 2) {
+                        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(row + q));
+                        cw[q] = v.x;
+                        cw[q + 1] = v.y;
+                    }
+                }
+            }
+            // ---- kernel 2: Bloom test of this half's slot (pre-state)
+            uint32_t ps = 0, word = 0;
+            bool init = true;
+            if (valid) {
+                ps = mod_z(fnv1a(id, hseed), p.geom);
+                init = sum_get(s_sum, ps >> 5);
+                if (init) word = __ldcg(bits + (ps >> 5));
+            }
             const uint32_t mybit = (word >> (ps & 31)) & 1u;
-            if (p.profile) asm volatile("" ::"r"(mybit));
+            if (p.profile) asm volatile("" ::"r"(mybit), "r"(cw[0]));
             BANG_CTA_PHASE(0)
             const uint32_t pbit = __shfl_xor_sync(kFull, mybit, 1);
             const uint32_t pps = __shfl_xor_sync(kFull, ps, 1);
@@ -211,7 +206,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             int wid = 0;
             uint32_t nid = 0;
             int ndeg = 0;
-            int n = 0;
             for (int pass = 0; pass < 2; ++pass) {
                 // ---- kernel 3: ADC, the two halves chained (engine.py:188-199)
                 float e[MH];
@@ -236,42 +230,18 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                     key = pack_key(acc, id);
                 }
                 surv = h == 1 && fresh && key < thr;  // ranks >= t are truncated (engine.py:213)
-                {
-                    const uint64_t wm = warp_min_u64(surv ? key : kSentinel);
-                    const unsigned sb = __ballot_sync(kFull, surv);
-                    const unsigned fb = __ballot_sync(kFull, fresh && h == 1);
-                    if (lane == 0) {
-                        s_m->wmin[warp] = wm;
-                        s_m->wcnt[warp] = __popc(sb);
-                        s_m->wfresh[warp] = __popc(fb);
-                    }
-                }
-                BANG_CTA_PHASE(2)
-                __syncthreads();
-                // ---- eager winner (engine.py:201-205) -> prefetch its row now
-                uint64_t best = kSentinel;
-                int F = 0, woff = 0;
-                n = 0;
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    best = s_m->wmin[w] < best ? s_m->wmin[w] : best;
-                    if (w < warp) woff += s_m->wcnt[w];
-                    n += s_m->wcnt[w];
-                    F += s_m->wfresh[w];
-                }
-                winner = best < head ? best : head;
-                if (winner != kSentinel) {
-                    wid = (int)key_id(winner);
-                    ndeg = p.deg[wid];
-                    nid = j < R ? (uint32_t)p.adj[(int64_t)wid * R + j] : 0u;
-                }
-                // ---- survivors -> s_nk (warp-aggregated)
-                const unsigned sball = __ballot_sync(kFull, surv);
-                if (surv) s_nk[woff + __popc(sball & lt)] = key;
-                // Bloom collision check: the fetch-or results are consumed only
-                // here, one ADC + reduction after they were issued
+                const uint64_t wm = warp_min_u64(surv ? key : kSentinel);
+                const unsigned sb = __ballot_sync(kFull, surv);
+                const unsigned fb = __ballot_sync(kFull, fresh && h == 1);
+                // Bloom collision check (fetch-or results) folded into the barrier
                 const uint32_t b = 1u << (ps & 31);
                 const bool coll = pass == 0 && do_atom && (old & b) && !(word & b);
+                if (lane == 0) {
+                    s_m->wmin[warp] = wm;
+                    s_m->wcnt[warp] = __popc(sb);
+                    s_m->wfresh[warp] = __popc(fb);
+                }
+                BANG_CTA_PHASE(2)
                 const int any_coll = __syncthreads_or(coll);
                 BANG_CTA_PHASE(3)
                 if (any_coll) {
@@ -310,13 +280,32 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                     __threadfence_block();
                     __syncthreads();
                     fresh = valid && s_fl[j];
-                    continue;  // redo the ADC, winner and survivors with the replayed fresh set
+                    continue;  // redo the ADC with the replayed fresh set
                 }
-                st_fresh += F;
                 break;
             }
+            // ---- eager winner (engine.py:201-205) -> prefetch its row now
+            uint64_t best = kSentinel;
+            int n = 0, F = 0, woff = 0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                best = s_m->wmin[w] < best ? s_m->wmin[w] : best;
+                if (w < warp) woff += s_m->wcnt[w];
+                n += s_m->wcnt[w];
+                F += s_m->wfresh[w];
+            }
+            winner = best < head ? best : head;
+            if (winner != kSentinel) {
+                wid = (int)key_id(winner);
+                ndeg = p.deg[wid];
+                nid = j < R ? (uint32_t)p.adj[(int64_t)wid * R + j] : 0u;
+            }
+            st_fresh += F;
+            // ---- survivors -> s_nk (warp-aggregated), sort (kernel 4a)
+            const unsigned sball = __ballot_sync(kFull, surv);
+            if (surv) s_nk[woff + __popc(sball & lt)] = key;
+            __syncthreads();
             BANG_CTA_PHASE(4)
-            // ---- sort survivors (kernel 4a)
             for (int q = tid; q < n; q += NT) {
                 const uint64_t k = s_nk[q];
                 int r = 0, i = 0;
@@ -327,13 +316,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             }
             __syncthreads();
             BANG_CTA_PHASE(5)
-            // ---- the winner's row: issue its code/Bloom loads now, so they
-            // land during the merge (this row's filter updates are ordered
-            // before them by the barriers above)
-            if (winner != kSentinel) {
-                id = nid;
-                issue_row(ndeg);
-            }
             // ---- kernel 4b: merge + truncate to t (engine.py:210-215)
             int wpos = t;
             if (winner != kSentinel)
@@ -383,6 +365,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             if (p.debug && tid == 0 && s_wl[upos] != winner) atomicAdd(p.counters + kCtrDebugFail, 1ull);
             u = (uint32_t)wid;
             deg = ndeg;
+            id = nid;
         }
         st_iters += iters;
         if (p.profile && tid == 0) s_m->t_ph = clock64();

@@ -117,6 +117,41 @@ def test_kernel3_adc_vectorised_code_rows():
             assert np.array_equal(got, want[rows == q])
 
 
+@pytest.mark.parametrize("d,m", [(128, 32), (96, 48), (20, 8)])
+def test_kernel3_adc_pairs_query_grouped(d, m):
+    """bang_adc_pairs_device (table built in shared memory per query) equals
+    the oracle's table + sequential ADC, including empty pair ranges."""
+    import torch
+    from paper_2401_11324_b200 import _lib
+    from paper_2401_11324_b200.tools.pq_train import encode, train_codebook
+    rng = np.random.default_rng(d + m)
+    n = 16_000
+    base = rng.normal(size=(n, d)).astype(np.float32)
+    cb = train_codebook(base, m=m, iters=3, seed=1)
+    codes = encode(base, cb).codes
+    graph = B.GraphIndex(np.zeros((n, 4), np.int32), np.zeros(n, np.int32), 0, 4)
+    s = B.GraphSearcher(k=1, t=4, mode="in_memory")
+    s.fit(base, graph=graph, codebook=cb, codes=B.CompressedVectors(codes))
+    nq = 37
+    q = rng.normal(size=(nq, d)).astype(np.float32)
+    counts = rng.integers(0, 700, size=nq)
+    counts[[3, 17]] = 0
+    off = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    ids = rng.integers(0, n, size=int(off[-1])).astype(np.uint32)
+    table = O.pq_table(q, cb.centroids, cb.subspace_sizes)
+    rows = np.repeat(np.arange(nq), counts)
+    want = O.pack_keys(O.adc(table, codes, rows, ids.astype(np.int64)), ids.astype(np.int64))
+    dev = torch.device("cuda", 0)
+    dq = torch.from_numpy(q).to(dev)
+    doff = torch.from_numpy(off).to(dev)
+    dids = torch.from_numpy(ids.view(np.int32)).to(dev)
+    dk = torch.empty(int(off[-1]), dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().bang_adc_pairs_device(s.index_.handle, _lib.ptr(dq), nq, _lib.ptr(doff), _lib.ptr(dids),
+                                                _lib.ptr(dk), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(dk.cpu().numpy().view(np.uint64), np.asarray(want, np.uint64))
+
+
 def test_kernel4_sort_and_merge_rows():
     g = gu.load("kernels.npz")
     assert np.array_equal(B.merge_sort_rows(g["keys"]), g["sorted"])
