@@ -31,6 +31,19 @@ CONFIGS = {
 }
 
 
+# Throughput-only shapes (BASELINE.json configs[3..4]; "C5:
+# seeded random 64-regular graph ... C5 has no recall").  The graph, codes,
+# codebook and u8 vectors are seeded random; the graph and vectors live in
+# pinned host memory (mode="pipelined").  C5's 1B x 64 adjacency (256 GB)
+# exceeds a single box's host RAM, so its shape is run at the largest n that
+# fits alongside C4.
+THROUGHPUT_CONFIGS = {
+    # name: (n, nq, dim, R, m, t, description)
+    "C4r": (100_000_000, 10_000, 128, 64, 32, 80,
+            "SIFT-shape 100Mx128 uint8, random 64-regular graph in pinned host memory "
+            "(throughput only, no recall), PQ 32 subspaces in HBM, 10K queries, t=80"),
+}
+
 EXACT_KNN_LIMIT = 2_000_000
 # search-based Vamana passes after the partitioned k-NN graph (n > EXACT_KNN_LIMIT):
 # (passes, worklist t).  At C3 two t=128 passes lift recall@10 at t=200 from
@@ -60,6 +73,46 @@ def refine_with_search(base, graph, codebook, codes, R, t=64, sigma=1.2, chunk=1
     deg_np = deg.to(torch.int32).cpu().numpy()
     adj_np[np.arange(R)[None, :] >= deg_np[:, None]] = -1
     return GraphIndex(adj_np, deg_np, graph.medoid, R, validate=False)
+
+
+def build_random_artifacts(name: str, seed: int = 0, nq_total: int | None = None, log=print):
+    """Seeded random index of a throughput-only shape (no ground truth)."""
+    import torch
+    from .._dev import torch_device
+    n, nq, dim, R, m, t, desc = THROUGHPUT_CONFIGS[name]
+    nq_total = nq_total or nq
+    dev = torch_device()
+    g = torch.Generator(device=dev).manual_seed(seed)
+    t0 = time.time()
+    chunk = 1 << 24
+    adj = np.empty((n, R), np.int32)
+    vec = np.empty((n, dim), np.uint8)
+    codes = np.empty((n, m), np.uint8)
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        a = torch.randint(0, n - 1, (hi - lo, R), generator=g, device=dev, dtype=torch.int64)
+        own = torch.arange(lo, hi, device=dev)[:, None]
+        a = torch.where(a >= own, a + 1, a)  # uniform over the other n-1 nodes: no self-loops
+        adj[lo:hi] = a.to(torch.int32).cpu().numpy()
+        vec[lo:hi] = torch.randint(0, 256, (hi - lo, dim), generator=g, device=dev, dtype=torch.int32).to(
+            torch.uint8).cpu().numpy()
+        codes[lo:hi] = torch.randint(0, 256, (hi - lo, m), generator=g, device=dev, dtype=torch.int32).to(
+            torch.uint8).cpu().numpy()
+    deg = np.full(n, R, np.int32)
+    queries = torch.randint(0, 256, (nq_total, dim), generator=g, device=dev, dtype=torch.int32).float().cpu().numpy()
+    sub = dim // m
+    cents = [torch.randint(0, 256, (256, sub), generator=g, device=dev, dtype=torch.int32).float().cpu().numpy()
+             for _ in range(m)]
+    # medoid: the point nearest the mean of a 1M-point sample (graph.py:107-115 on a sample)
+    samp = torch.from_numpy(vec[:: max(1, n // 1_000_000)]).to(dev).double()
+    medoid = int(((samp - samp.mean(0)) ** 2).sum(1).argmin().item()) * max(1, n // 1_000_000)
+    log(f"[bench_data] {name}: random artifacts in {time.time() - t0:.1f}s")
+    return dict(base=vec, queries=queries,
+                graph=GraphIndex(adj, deg, medoid, R, validate=False),
+                codebook=PQCodebook(dim=dim, subspace_sizes=[sub] * m, centroids=cents),
+                codes=CompressedVectors(codes), gt_ids=None, gt_dists=None,
+                meta=dict(desc=desc, n=n, dim=dim, dtype="u8", R=R, m=m, clusters=0, t=t,
+                          throughput_only=True))
 
 
 def _key(name, seed, nq_total):
@@ -113,6 +166,8 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
     from .groundtruth import brute_force_knn
     from .pq_train import encode, train_codebook
 
+    if name in THROUGHPUT_CONFIGS:
+        return build_random_artifacts(name, seed, nq_total, log)
     n, nq, dim, dt, clusters, R, m, desc = CONFIGS[name]
     nq_total = nq_total or nq
     meta = dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters)
