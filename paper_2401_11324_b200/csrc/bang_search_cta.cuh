@@ -34,6 +34,36 @@ struct CtaMisc {
 };
 static_assert(sizeof(CtaMisc) <= 256, "CtaMisc must fit its 256-byte smem slot");
 
+// Kernel 5 with the visited rows staged through shared memory: the CTA copies
+// a chunk of rows with coalesced 16-byte loads (one PCIe read request per
+// 128 B when the vectors live in pinned, mapped host memory, instead of one
+// per 4-byte word), then each thread sums its row exactly as exact_sq_dist
+// does on the original (engine.py:48-51; same arithmetic, same order).
+template <int NT>
+__device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32_t *log, int iters,
+                                              const float *s_q, uint8_t *stage, int stage_bytes,
+                                              uint64_t *rr) {
+    const int tid = threadIdx.x;
+    const int rb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);  // a multiple of 16 (caller)
+    const int upr = rb / 16;
+    const int ch = stage_bytes / rb;
+    const uint8_t *vec = static_cast<const uint8_t *>(p.vectors);
+    for (int base = 0; base < iters; base += ch) {
+        const int nr = min(ch, iters - base);
+        for (int u = tid; u < nr * upr; u += NT) {
+            const int r = u / upr, c = u - r * upr;
+            const uint32_t node = (uint32_t)__ldcg(log + base + r);
+            reinterpret_cast<uint4 *>(stage)[u] = reinterpret_cast<const uint4 *>(vec + (int64_t)node * rb)[c];
+        }
+        __syncthreads();
+        for (int i = tid; i < nr; i += NT) {
+            const uint32_t node = (uint32_t)__ldcg(log + base + i);
+            rr[base + i] = pack_key(exact_sq_dist(stage, p.vec_dtype, p.dim, i, s_q), node);
+        }
+        __syncthreads();
+    }
+}
+
 template <int NT, int SUB, int MV>
 // 768/NT CTAs per SM: 6 queries of 128 threads (R <= 64) fit the register file at <= 80 regs;
 // at m = 48 the 48 KB table caps residency at 4 per SM, so allow 128 regs
@@ -389,9 +419,15 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             // kernel 5: exact distances of the visit log, then top-k (warp 0)
             __threadfence_block();
             __syncthreads();
-            for (int i = tid; i < iters; i += NT) {
-                const uint32_t node = (uint32_t)__ldcg(log + i);
-                rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+            const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
+            if (rowb % 16 == 0 && rowb <= M * 256 * 4) {
+                // the table is dead until the next query: stage rows in its place
+                rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), M * 256 * 4, rr);
+            } else {
+                for (int i = tid; i < iters; i += NT) {
+                    const uint32_t node = (uint32_t)__ldcg(log + i);
+                    rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+                }
             }
             st_rr += (tid == 0) ? iters : 0;
             __threadfence_block();

@@ -348,6 +348,24 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
+@pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
+    (14, 16_000, 128, 64, 32, 48, np.uint8),
+    (15, 16_000, 96, 64, 48, 64, np.float32),
+])
+def test_pipelined_cta_kernel_matches_oracle(seed, n, d, R, m, t, dtype):
+    """Graph + vectors in pinned, mapped host memory (mode="pipelined"), CTA
+    kernel with the staged re-rank: identical to the oracle."""
+    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
+    s = B.GraphSearcher(k=10, t=t, mode="pipelined", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=10, t=t, bloom_entries=399_887, threads=8)
+    res = s.search(q)
+    assert s.last_stats()["kernel"] == 2
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+
+
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank,nq", [
     (5, 20_000, 96, 64, 48, 32, np.float32, 1021, True, 500),     # collision-heavy Bloom: replay path
     (6, 20_000, 128, 64, 32, 40, np.uint8, 4099, False, 300),     # no re-rank: wl[0:k] outputs
