@@ -194,7 +194,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
     ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
-    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool", "smem-table-nofat", "fat"))
+    ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table", "pool", "smem-table-nofat", "fat", "pipelined-rows"))
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))

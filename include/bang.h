@@ -57,6 +57,7 @@ typedef int32_t bang_status;
 #define BANG_QUERY_POOL 512    /* lockstep query pool per CTA, CTA-shared codebook ADC        */
 #define BANG_NO_POOL 1024      /* never pick the query-pool kernel automatically               */
 #define BANG_NO_FAT 2048       /* do not use the fat-row (inline neighbour codes) CTA kernel  */
+#define BANG_PIPELINE_ROWS 4096 /* CTA kernel with the next row's loads issued during the merge */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
 

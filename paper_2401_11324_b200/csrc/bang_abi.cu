@@ -21,6 +21,7 @@
 #include "bang_search_cta.cuh"
 #include "bang_search_pool.cuh"
 #include "bang_search_fat.cuh"
+#include "bang_search_ctapipe.cuh"
 
 using namespace bang;
 
@@ -135,6 +136,7 @@ struct Plan {
     bool cta_kernel = false;  // search_cta_kernel (one CTA per query, smem table)
     bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
     bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
+    bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
     int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
     int nt = 0;               // threads per CTA of the CTA kernel
@@ -192,6 +194,20 @@ const void *pick_fat_kernel(int nt, int sub, int mv) {
     if (nt == N && sub == S && mv == V) return fat_kernel_ptr<N, S, V>();
     BANG_F(64, 4, 2) BANG_F(128, 4, 2) BANG_F(64, 2, 3) BANG_F(128, 2, 3)
 #undef BANG_F
+    return nullptr;
+}
+
+template <int NT, int SUB, int MV>
+const void *pipe_kernel_ptr() {
+    return reinterpret_cast<const void *>(&search_ctapipe_kernel<NT, SUB, MV>);
+}
+
+const void *pick_pipe_kernel(int nt, int sub, int mv) {
+#define BANG_Q(N, S, V) \
+    if (nt == N && sub == S && mv == V) return pipe_kernel_ptr<N, S, V>();
+    BANG_Q(64, 4, 2) BANG_Q(128, 4, 2) BANG_Q(256, 4, 2) BANG_Q(64, 2, 3) BANG_Q(128, 2, 3) BANG_Q(256, 2, 3)
+    BANG_Q(64, 0, 2) BANG_Q(128, 0, 2) BANG_Q(256, 0, 2) BANG_Q(64, 0, 3) BANG_Q(128, 0, 3) BANG_Q(256, 0, 3)
+#undef BANG_Q
     return nullptr;
 }
 
@@ -350,6 +366,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_sum = take(4LL * pl.sum_words);
         pl.off_tab = take(tab_bytes);
         pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
+        pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
         if (pl.fat_kernel) {
             pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
             pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
@@ -359,7 +376,9 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.warps = pl.nt / 32;
         pl.smem = pl.per_warp;
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
-        const void *kc = pl.fat_kernel ? pick_fat_kernel(pl.nt, pl.sub, pl.mv) : pick_cta_kernel(pl.nt, pl.sub, pl.mv);
+        const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
+                         : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
+                                          : pick_cta_kernel(pl.nt, pl.sub, pl.mv);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
         int per_sm = 0;
@@ -470,6 +489,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
         return BANG_OK;
     }
     const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);
@@ -537,7 +557,7 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
     ix->stats.warps_per_cta = pl.warps;
     ix->stats.ctas = pl.ctas;
     ix->stats.adc_variant = pl.variant;
-    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
+    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.pipe_kernel ? 5 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
     ix->last_nq = nq;
     ix->last_log_cap = cap;
     ix->last_has_table = d_table != nullptr;

@@ -322,7 +322,9 @@ class GraphSearcher(BaseEstimator):
                   # lockstep query pool per CTA with the CTA-shared codebook
                   "pool": _lib.QUERY_POOL,
                   # CTA per query without the fat-row layout (ids and codes read separately)
-                  "smem-table-nofat": _lib.TABLE_SMEM | _lib.NO_FAT}
+                  "smem-table-nofat": _lib.TABLE_SMEM | _lib.NO_FAT,
+                  # CTA per query with the next row's code/Bloom loads issued during the merge
+                  "pipelined-rows": _lib.TABLE_SMEM | _lib.PIPELINE_ROWS}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):
