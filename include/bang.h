@@ -117,7 +117,9 @@ void bang_index_destroy(bang_index *index);
 /* device ordinal, n, m, dim, R of the handle */
 bang_status bang_index_info(const bang_index *index, int32_t *device, int64_t *n, int32_t *m,
                             int32_t *dim, int32_t *R);
-/* Device pointers owned by the handle (for the per-kernel entries). */
+/* Device pointers owned by the handle (for the per-kernel entries).  With
+ * BANG_GRAPH_HOST_MAPPED and R % 4 == 0 the adjacency rows have a stride of
+ * R + 4 int32: a 16-byte [deg, 0, 0, 0] header precedes each row. */
 bang_status bang_index_device_ptrs(const bang_index *index, const uint8_t **codes,
                                    const float **centroids, const int32_t **adjacency,
                                    const int32_t **degrees, const void **vectors);

@@ -93,6 +93,9 @@ struct bang_index {
     float *centroids = nullptr;
     int32_t *d_sub_off = nullptr, *d_sub_size = nullptr;
     int32_t *adj = nullptr, *deg = nullptr;
+    int32_t *adj_alloc = nullptr;  // allocation base (host-mapped rows carry a header)
+    int64_t adj_stride = 0;
+    bool row_hdr = false;
     void *vectors = nullptr;
     bool host_graph = false;
     // fat rows (bang_search_fat.cuh): ids + inline neighbour codes, HBM only
@@ -137,6 +140,7 @@ struct Plan {
     bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
     bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
     bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
+    int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
     int nt = 0;               // threads per CTA of the CTA kernel
@@ -367,6 +371,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_tab = take(tab_bytes);
         pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
         pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
+        if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
         if (pl.fat_kernel) {
             pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
             pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
@@ -426,6 +431,9 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.sub_size = ix->d_sub_size;
     p.table = d_table;
     p.adj = ix->adj;
+    p.adj_stride = ix->adj_stride;
+    p.row_hdr = ix->row_hdr && pl.cta_kernel && !pl.fat_kernel && !pl.pipe_kernel ? 1 : 0;
+    p.off_row = pl.off_row;
     p.deg = ix->deg;
     p.vectors = ix->vectors;
     p.queries = d_queries;
@@ -690,13 +698,30 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
         // one pinned, mapped host copy read by the kernel over PCIe (the
         // paper's host-resident graph)
         ix->host_graph = true;
-        CUX(cudaHostAlloc(reinterpret_cast<void **>(&ix->adj), adj_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        // Rows get a 16-byte header [deg, 0, 0, 0] when R % 4 == 0, so the
+        // one-hop-ahead fetch is ONE coalesced read of degree + ids (fewer,
+        // larger PCIe read requests than per-thread 4-byte reads)
+        ix->row_hdr = R % 4 == 0;
+        ix->adj_stride = ix->row_hdr ? R + 4 : R;
+        const size_t rows_bytes = (size_t)n * ix->adj_stride * 4;
+        CUX(cudaHostAlloc(reinterpret_cast<void **>(&ix->adj_alloc), rows_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
         CUX(cudaHostAlloc(reinterpret_cast<void **>(&ix->deg), deg_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
         CUX(cudaHostAlloc(&ix->vectors, vec_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
-        memcpy(ix->adj, adjacency, adj_bytes);
+        ix->adj = ix->adj_alloc + (ix->row_hdr ? 4 : 0);
+        if (ix->row_hdr) {
+            for (int64_t i = 0; i < n; ++i) {
+                int32_t *row = ix->adj_alloc + i * ix->adj_stride;
+                row[0] = degrees[i];
+                row[1] = row[2] = row[3] = 0;
+                memcpy(row + 4, adjacency + i * R, (size_t)R * 4);
+            }
+        } else {
+            memcpy(ix->adj, adjacency, adj_bytes);
+        }
         memcpy(ix->deg, degrees, deg_bytes);
         memcpy(ix->vectors, vectors, vec_bytes);
     } else if (graph_placement == BANG_GRAPH_HBM) {
+        ix->adj_stride = R;
         CUX(cudaMalloc(&ix->adj, adj_bytes));
         CUX(cudaMalloc(&ix->deg, deg_bytes));
         CUX(cudaMalloc(&ix->vectors, vec_bytes));
@@ -739,7 +764,7 @@ void bang_index_destroy(bang_index *ix) {
     cudaFree(ix->d_sub_off);
     cudaFree(ix->d_sub_size);
     if (ix->host_graph) {
-        cudaFreeHost(ix->adj);
+        cudaFreeHost(ix->adj_alloc);
         cudaFreeHost(ix->deg);
         cudaFreeHost(ix->vectors);
     } else {

@@ -74,6 +74,11 @@ struct SearchParams {
     const uint8_t *fat;
     int64_t fat_stride;
     int32_t fat_code_off, off_dup;
+    // adjacency row i starts at adj + i * adj_stride.  row_hdr: host-mapped
+    // rows carry a 16-byte header [deg, 0, 0, 0] at adj - 4 so one coalesced
+    // read fetches degree + ids (search_cta_kernel stages it at off_row)
+    int64_t adj_stride;
+    int32_t row_hdr, off_row;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
 #pragma unroll
         for (int k = 0; k < NPL; ++k) {
             const int c = lane + 32 * k;
-            ids[k] = c < R ? (uint32_t)p.adj[(int64_t)u * R + c] : 0u;
+            ids[k] = c < R ? (uint32_t)p.adj[(int64_t)u * p.adj_stride + c] : 0u;
         }
         // log rows follow the pass order when a query map is given (retry pass)
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
 #pragma unroll
                 for (int k = 0; k < NPL; ++k) {
                     const int c = lane + 32 * k;
-                    nids[k] = c < R ? (uint32_t)p.adj[(int64_t)w * R + c] : 0u;
+                    nids[k] = c < R ? (uint32_t)p.adj[(int64_t)w * p.adj_stride + c] : 0u;
                 }
             } else {
 #pragma unroll

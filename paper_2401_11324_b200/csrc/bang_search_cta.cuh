@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         int deg = p.deg[u];
-        uint32_t id = j < R ? (uint32_t)p.adj[(int64_t)u * R + j] : 0u;
+        uint32_t id = j < R ? (uint32_t)p.adj[(int64_t)u * p.adj_stride + j] : 0u;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
         __syncthreads();
@@ -325,10 +325,19 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                 F += s_m->wfresh[w];
             }
             winner = best < head ? best : head;
+            // host-mapped rows: warp 0 fetches [deg | ids] in one coalesced read,
+            // staged to smem at the end of the merge (PCIe: few large requests)
+            uint4 rowv = make_uint4(0u, 0u, 0u, 0u);
+            const int nchunk = (R + 4) >> 2;
             if (winner != kSentinel) {
                 wid = (int)key_id(winner);
-                ndeg = p.deg[wid];
-                nid = j < R ? (uint32_t)p.adj[(int64_t)wid * R + j] : 0u;
+                if (p.row_hdr) {
+                    if (warp == 0 && lane < nchunk)
+                        rowv = reinterpret_cast<const uint4 *>(p.adj - 4 + (int64_t)wid * p.adj_stride)[lane];
+                } else {
+                    ndeg = p.deg[wid];
+                    nid = j < R ? (uint32_t)p.adj[(int64_t)wid * p.adj_stride + j] : 0u;
+                }
             }
             st_fresh += F;
             // ---- survivors -> s_nk (warp-aggregated), sort (kernel 4a)
@@ -387,8 +396,15 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                 }
             }
             cnt = min(t, cnt + n);
+            if (p.row_hdr && winner != kSentinel && warp == 0 && lane < nchunk)
+                reinterpret_cast<uint4 *>(smem + p.off_row)[lane] = rowv;
             __syncthreads();
             BANG_CTA_PHASE(6)
+            if (p.row_hdr && winner != kSentinel) {
+                const int32_t *sr = reinterpret_cast<const int32_t *>(smem + p.off_row);
+                ndeg = sr[0];
+                nid = j < R ? (uint32_t)sr[4 + j] : 0u;
+            }
             // ---- converge (engine.py:217-236)
             if (wpos >= t) break;
             upos = wpos;

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_ctapipe
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         int deg = p.deg[u];
-        uint32_t id = j < R ? (uint32_t)p.adj[(int64_t)u * R + j] : 0u;
+        uint32_t id = j < R ? (uint32_t)p.adj[(int64_t)u * p.adj_stride + j] : 0u;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
         // Next-row issue: this half's code bytes, Bloom slot, summary bit and
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_ctapipe
                 if (winner != kSentinel) {
                     wid = (int)key_id(winner);
                     ndeg = p.deg[wid];
-                    nid = j < R ? (uint32_t)p.adj[(int64_t)wid * R + j] : 0u;
+                    nid = j < R ? (uint32_t)p.adj[(int64_t)wid * p.adj_stride + j] : 0u;
                 }
                 // ---- survivors -> s_nk (warp-aggregated)
                 const unsigned sball = __ballot_sync(kFull, surv);

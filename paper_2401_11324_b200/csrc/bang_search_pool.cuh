@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
             c->deg = p.deg[p.medoid];
         }
         uint32_t *adj = S_adj(s);
-        for (int j = lane; j < RPAD; j += 32) adj[j] = j < R ? (uint32_t)p.adj[(int64_t)p.medoid * R + j] : 0u;
+        for (int j = lane; j < RPAD; j += 32) adj[j] = j < R ? (uint32_t)p.adj[(int64_t)p.medoid * p.adj_stride + j] : 0u;
         __syncwarp();
     };
 
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kPoolThreads, 1) search_pool_kernel(const Sear
 #pragma unroll
                     for (int r = 0; r < NPL; ++r) {
                         const int j = lane + 32 * r;
-                        na[r] = j < R ? (uint32_t)p.adj[(int64_t)w * R + j] : 0u;
+                        na[r] = j < R ? (uint32_t)p.adj[(int64_t)w * p.adj_stride + j] : 0u;
                     }
                 }
                 __syncwarp();

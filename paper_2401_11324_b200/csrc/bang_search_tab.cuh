@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256, 1) search_tab_kernel(const SearchParams p
 #pragma unroll
         for (int k = 0; k < NPL; ++k) {
             const int c = lane + 32 * k;
-            ids[k] = c < R ? (uint32_t)p.adj[(int64_t)u * R + c] : 0u;
+            ids[k] = c < R ? (uint32_t)p.adj[(int64_t)u * p.adj_stride + c] : 0u;
         }
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256, 1) search_tab_kernel(const SearchParams p
 #pragma unroll
                         for (int k = 0; k < NPL; ++k) {
                             const int c = lane + 32 * k;
-                            nids[k] = c < R ? (uint32_t)p.adj[(int64_t)wid * R + c] : 0u;
+                            nids[k] = c < R ? (uint32_t)p.adj[(int64_t)wid * p.adj_stride + c] : 0u;
                         }
                     }
                 }

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--passes", type=int, default=2)
     ap.add_argument("--refine-t", type=int, default=128)
     ap.add_argument("--ts", default="64,128,200")
+    ap.add_argument("--sigma", type=float, default=1.2)
+    ap.add_argument("--modes", default="in_memory,exact_distance")
     args = ap.parse_args()
     import torch
     from paper_2401_11324_b200 import GraphSearcher
@@ -35,7 +37,7 @@ def main():
 
     def evaluate(graph, tag):
         out = {"graph": tag}
-        for mode in ("in_memory", "exact_distance"):
+        for mode in args.modes.split(","):
             s = GraphSearcher(k=10, t=max(ts), mode=mode, batch_size=10_000)
             s.fit(art["base"], graph=graph, codebook=art["codebook"], codes=art["codes"])
             for t in ts:
@@ -50,10 +52,11 @@ def main():
     evaluate(g, "built")
     for p in range(args.passes):
         t0 = time.time()
-        g = bd.refine_with_search(art["base"], g, art["codebook"], art["codes"], R, t=args.refine_t, log=log)
+        g = bd.refine_with_search(art["base"], g, art["codebook"], art["codes"], R, t=args.refine_t,
+                                  sigma=args.sigma, log=log)
         log(f"pass {p + 1}: {time.time() - t0:.1f}s")
         torch.cuda.empty_cache()
-        evaluate(g, f"+{p + 1} pass(es) t={args.refine_t}")
+        evaluate(g, f"+{p + 1} pass(es) t={args.refine_t} sigma={args.sigma}")
 
 
 if __name__ == "__main__":
