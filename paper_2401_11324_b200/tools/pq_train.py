@@ -40,7 +40,10 @@ def train_codebook(base, m: int, iters: int = 25, seed: int = 0, sample: int = 2
     sub = _subspace_views(xs, sizes)  # (m, ns, w)
     ns = sub.shape[1]
     k = CENTROIDS_PER_SUBSPACE
-    init = torch.from_numpy(rng.choice(ns, size=(m, k), replace=ns < k)).to(dev)
+    if ns >= m * k:
+        init = torch.from_numpy(rng.choice(ns, size=(m, k), replace=False)).to(dev)
+    else:  # small training sets: k distinct rows per subspace, drawn independently
+        init = torch.from_numpy(np.stack([rng.choice(ns, size=k, replace=ns < k) for _ in range(m)])).to(dev)
     cents = torch.gather(sub, 1, init[:, :, None].expand(m, k, sub.shape[2])).clone()
     for _ in range(iters):
         d = (sub.square().sum(-1, keepdim=True) - 2 * torch.bmm(sub, cents.transpose(1, 2))
