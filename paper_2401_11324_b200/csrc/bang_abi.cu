@@ -173,13 +173,14 @@ const void *pick_tab_kernel(int npl, int sub, int mv) {
 }
 
 template <int NT, int SUB, int MV>
-const void *cta_kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV>);
+const void *cta_kernel_ptr(bool hdr) {
+    return hdr ? reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV, true>)
+               : reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV, false>);
 }
 
-const void *pick_cta_kernel(int nt, int sub, int mv) {
+const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr = false) {
 #define BANG_C(N, S, V) \
-    if (nt == N && sub == S && mv == V) return cta_kernel_ptr<N, S, V>();
+    if (nt == N && sub == S && mv == V) return cta_kernel_ptr<N, S, V>(hdr);
     BANG_C(64, 4, 2) BANG_C(128, 4, 2) BANG_C(256, 4, 2)
     BANG_C(64, 2, 3) BANG_C(128, 2, 3) BANG_C(256, 2, 3)
     BANG_C(64, 0, 2) BANG_C(128, 0, 2) BANG_C(256, 0, 2)
@@ -383,7 +384,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
         const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                          : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                                          : pick_cta_kernel(pl.nt, pl.sub, pl.mv);
+                                          : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
         int per_sm = 0;
@@ -498,7 +499,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     }
     const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                      : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv, p.row_hdr != 0)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};

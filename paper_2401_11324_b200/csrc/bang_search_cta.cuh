@@ -64,7 +64,8 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
     }
 }
 
-template <int NT, int SUB, int MV>
+template <int NT, int SUB, int MV, bool HDR>
+// HDR: host-mapped rows with a [deg,0,0,0] header (p.row_hdr), fetched by warp 0
 // 768/NT CTAs per SM: 6 queries of 128 threads (R <= 64) fit the register file at <= 80 regs;
 // at m = 48 the 48 KB table caps residency at 4 per SM, so allow 128 regs
 __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_kernel(const SearchParams p) {
@@ -331,7 +332,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             const int nchunk = (R + 4) >> 2;
             if (winner != kSentinel) {
                 wid = (int)key_id(winner);
-                if (p.row_hdr) {
+                if (HDR) {
                     if (warp == 0 && lane < nchunk)
                         rowv = reinterpret_cast<const uint4 *>(p.adj - 4 + (int64_t)wid * p.adj_stride)[lane];
                 } else {
@@ -396,11 +397,11 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                 }
             }
             cnt = min(t, cnt + n);
-            if (p.row_hdr && winner != kSentinel && warp == 0 && lane < nchunk)
+            if (HDR && winner != kSentinel && warp == 0 && lane < nchunk)
                 reinterpret_cast<uint4 *>(smem + p.off_row)[lane] = rowv;
             __syncthreads();
             BANG_CTA_PHASE(6)
-            if (p.row_hdr && winner != kSentinel) {
+            if (HDR && winner != kSentinel) {
                 const int32_t *sr = reinterpret_cast<const int32_t *>(smem + p.off_row);
                 ndeg = sr[0];
                 nid = j < R ? (uint32_t)sr[4 + j] : 0u;

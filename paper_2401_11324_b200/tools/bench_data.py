@@ -46,9 +46,10 @@ THROUGHPUT_CONFIGS = {
 
 EXACT_KNN_LIMIT = 2_000_000
 # search-based Vamana passes after the partitioned k-NN graph (n > EXACT_KNN_LIMIT):
-# (passes, worklist t).  At C3 two t=128 passes lift recall@10 at t=200 from
-# 0.846 to 0.915 (profiles/r01/c3_graph_study.jsonl).
-REFINE = (2, 128)
+# the worklist t of each pass.  At C3 two t=128 passes lift recall@10 at t=200
+# from 0.846 to 0.911, a third at t=200 to 0.918 (0.897 at t=160)
+# (profiles/r01/c3_graph_study*.jsonl).
+REFINE = (128, 128, 200)
 
 
 def refine_with_search(base, graph, codebook, codes, R, t=64, sigma=1.2, chunk=1 << 20, log=print):
@@ -191,8 +192,8 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         # partitioned k-NN graph -> one search-based Vamana pass with the
         # B200 search itself (the reference's builder, graph.py:251-344,
         # inserts by greedy search too)
-        for _ in range(REFINE[0]):
-            graph = refine_with_search(base, graph, cb, codes, R, t=REFINE[1], log=log)
+        for t_ref in REFINE:
+            graph = refine_with_search(base, graph, cb, codes, R, t=t_ref, log=log)
         t2 += time.time() - t3
         t3 = time.time()
     gt_ids, gt_d = brute_force_knn(base, queries, 10)
