@@ -106,6 +106,8 @@ struct bang_index {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int sm_count = 148;
     int max_smem = 227 * 1024;
+    int64_t persist_max = 0, window_max = 0;  // L2 persistence limits of the device
+    size_t persist_set = 0;
     // workspace
     DevBuf<float> q, table;
     DevBuf<int32_t> ids, iters, log, overflow, qmap;
@@ -503,6 +505,35 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
+    // The per-slot Bloom filters (C2: 888 x 50 KB, C3: 592 x 50 KB) are the
+    // search's only re-read random working set; the code/adjacency/vector
+    // gathers stream past them.  Mark the filters L2-persisting for this
+    // launch (BANG_NO_L2_PERSIST=1 disables) so Bloom words stay L2 hits.
+    const char *nopersist = getenv("BANG_NO_L2_PERSIST");
+    const size_t bloom_bytes = (size_t)pl.slots * pl.bloom_stride * 4;
+    if (ix->persist_max > 0 && !(nopersist && *nopersist == '1')) {
+        const size_t win = std::min<size_t>(bloom_bytes, (size_t)ix->persist_max);
+        if (ix->persist_set != win) {
+            CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win));
+            ix->persist_set = win;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(pl.ctas);
+        cfg.blockDim = dim3(pl.warps * 32);
+        cfg.dynamicSmemBytes = (size_t)pl.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr{};
+        attr.id = cudaLaunchAttributeAccessPolicyWindow;
+        attr.val.accessPolicyWindow.base_ptr = ix->bloom.p;
+        attr.val.accessPolicyWindow.num_bytes = std::min<size_t>(bloom_bytes, (size_t)ix->window_max);
+        attr.val.accessPolicyWindow.hitRatio = 1.0f;
+        attr.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelExC(&cfg, kfn, args));
+        return BANG_OK;
+    }
     CU(cudaLaunchKernel(kfn, dim3(pl.ctas), dim3(pl.warps * 32), args, (size_t)pl.smem, st));
     return BANG_OK;
 }
@@ -681,6 +712,8 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
     CUX(cudaGetDeviceProperties(&prop, device));
     ix->sm_count = prop.multiProcessorCount;
     ix->max_smem = (int)prop.sharedMemPerBlockOptin;
+    ix->persist_max = prop.persistingL2CacheMaxSize;
+    ix->window_max = prop.accessPolicyMaxWindowSize;
     CUX(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) CUX(cudaEventCreate(&e));
     const size_t elem = vec_dtype == BANG_VEC_F32 ? 4 : 1;

@@ -446,24 +446,20 @@ __device__ __forceinline__ float exact_sq_dist(const void *__restrict__ vectors,
 }
 
 // ------------------------------------------------------- sorted arrays
-// number of entries of sorted a[0, n) strictly below x
+// number of entries of sorted a[0, n) strictly below x.  Binary lifting:
+// the trip count depends on n only, so lanes searching different keys of
+// the same array never diverge.
 __device__ __forceinline__ int lower_bound_u64(const uint64_t *a, int n, uint64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
+    int lo = 0;
+    for (int step = n > 0 ? 1 << (31 - __clz(n)) : 0; step > 0; step >>= 1)
+        if (lo + step <= n && a[lo + step - 1] < x) lo += step;
     return lo;
 }
 // number of entries of sorted a[0, n) at or below x
 __device__ __forceinline__ int upper_bound_u64(const uint64_t *a, int n, uint64_t x) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid + 1;
-        else hi = mid;
-    }
+    int lo = 0;
+    for (int step = n > 0 ? 1 << (31 - __clz(n)) : 0; step > 0; step >>= 1)
+        if (lo + step <= n && a[lo + step - 1] <= x) lo += step;
     return lo;
 }
 
