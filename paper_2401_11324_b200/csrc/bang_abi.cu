@@ -1068,7 +1068,10 @@ bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_
     cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : ix->stream;
     const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
     const int sub = ix->uniform_sub;
-    const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + ix->dim);
+    // table + query (+ per-warp double-buffered code-row stages, vector path)
+    const bool vec = (sub == 4 && mv == 2) || (sub == 2 && mv == 3);
+    const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + align_up(ix->dim, 4)) +
+                        (vec ? (size_t)8 * 2 * 32 * ix->m : 0);
     if (smem > (size_t)ix->max_smem) return fail(BANG_E_PARAM, "table of m=%d does not fit in shared memory", ix->m);
     auto launch = [&](const void *fn) -> bang_status {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

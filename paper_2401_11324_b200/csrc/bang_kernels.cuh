@@ -14,6 +14,8 @@
 
 #include "bang_device.cuh"
 
+#include <cuda_pipeline.h>
+
 namespace bang {
 
 // counters[] slots of the fused kernel
@@ -840,25 +842,50 @@ __global__ void __launch_bounds__(256) adc_pairs_kernel(const float *__restrict_
         __syncthreads();
         const int64_t lo = off[q], hi = off[q + 1];
         if constexpr (MV > 0) {
-            // two pairs per thread per step: both code rows in flight together
-            for (int64_t i = lo + tid; i < hi; i += 2 * nt) {
-                const int64_t i1 = i + nt;
-                const bool has1 = i1 < hi;
-                const uint32_t n0 = __ldg(ids + i), n1 = has1 ? __ldg(ids + i1) : n0;
-                uint4 c0[MV], c1[MV];
+            // Per warp, rounds of 32 pairs: the 32 code rows are copied into
+            // the warp's smem stage by cp.async with MV consecutive lanes per
+            // row (coalesced 16-byte pieces, no registers held), double
+            // buffered so round r+1's rows are in flight while round r sums.
+            constexpr int M = 16 * MV;
+            const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+            uint8_t *stage = reinterpret_cast<uint8_t *>(s_q + ((dim + 3) & ~3)) + (size_t)warp * 2 * 32 * M;
+            const int64_t nround = (hi - lo + 31) / 32;
+            auto issue = [&](int64_t r, int buf) -> uint32_t {
+                const int64_t base = lo + r * 32;
+                const uint32_t my = base + lane < hi ? __ldg(ids + base + lane) : 0u;
 #pragma unroll
                 for (int v = 0; v < MV; ++v) {
-                    c0[v] = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)n0 * (16 * MV)) + v);
-                    c1[v] = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)n1 * (16 * MV)) + v);
+                    const int ci = v * 32 + lane, row = ci / MV, part = ci - row * MV;
+                    const uint32_t rid = __shfl_sync(kFull, my, row);
+                    if (base + row < hi)
+                        __pipeline_memcpy_async(stage + (size_t)buf * 32 * M + ci * 16,
+                                                codes + (int64_t)rid * M + part * 16, 16);
                 }
-                float a0 = 0.0f, a1 = 0.0f;
+                __pipeline_commit();
+                return my;
+            };
+            int64_t r = warp;
+            uint32_t cur = r < nround ? issue(r, 0) : 0u;
+            for (int k = 0; r < nround; ++k, r += nw) {
+                const int64_t rn = r + nw;
+                uint32_t nxt = 0u;
+                if (rn < nround) {
+                    nxt = issue(rn, (k + 1) & 1);
+                    __pipeline_wait_prior(1);
+                } else {
+                    __pipeline_wait_prior(0);
+                }
+                __syncwarp();
+                const int64_t i = lo + r * 32 + lane;
+                if (i < hi) {
+                    const uint4 *row = reinterpret_cast<const uint4 *>(stage + (size_t)(k & 1) * 32 * M + lane * M);
+                    float a = 0.0f;
 #pragma unroll
-                for (int v = 0; v < MV; ++v) {
-                    a0 = adc_tab_stage16(a0, s_tab, 16 * v, c0[v]);
-                    a1 = adc_tab_stage16(a1, s_tab, 16 * v, c1[v]);
+                    for (int v = 0; v < MV; ++v) a = adc_tab_stage16(a, s_tab, 16 * v, row[v]);
+                    keys[i] = pack_key(a, cur);
                 }
-                keys[i] = pack_key(a0, n0);
-                if (has1) keys[i1] = pack_key(a1, n1);
+                __syncwarp();  // this buffer is refilled two rounds later
+                cur = nxt;
             }
         } else {
             for (int64_t i = lo + tid; i < hi; i += nt) {
