@@ -51,7 +51,10 @@ class VisitLogs(Sequence):
         self._base = [0]
         for offs, flat in parts:
             self._offs.append(np.asarray(offs, np.int64))
-            self._flat.append(np.asarray(flat).astype(np.int64, copy=False))
+            # ids stay in the device's int32 until a log is read: logs[i]
+            # returns int64 like the reference, without widening 10^6+ ids
+            # per batch up front
+            self._flat.append(np.asarray(flat))
             self._base.append(self._base[-1] + len(offs) - 1)
 
     def __len__(self):
@@ -68,7 +71,7 @@ class VisitLogs(Sequence):
         p = int(np.searchsorted(self._base, i, side="right")) - 1
         j = i - self._base[p]
         offs = self._offs[p]
-        return self._flat[p][offs[j]:offs[j + 1]]
+        return self._flat[p][offs[j]:offs[j + 1]].astype(np.int64)
 
     def __eq__(self, other):
         return len(self) == len(other) and all(np.array_equal(a, b) for a, b in zip(self, other))
@@ -76,13 +79,14 @@ class VisitLogs(Sequence):
     def csr(self):
         """(offsets (n+1,) int64, ids int64): all logs as one CSR pair."""
         if len(self._offs) == 1:
-            return self._offs[0], self._flat[0]
+            return self._offs[0], self._flat[0].astype(np.int64, copy=False)
         offs, flats, base = [np.zeros(1, np.int64)], [], 0
         for o, f in zip(self._offs, self._flat):
             offs.append(o[1:] - o[0] + base)
             flats.append(f[o[0]:o[-1]])
             base += int(o[-1] - o[0])
-        return np.concatenate(offs), (np.concatenate(flats) if flats else np.zeros(0, np.int64))
+        return np.concatenate(offs), (np.concatenate(flats).astype(np.int64, copy=False) if flats
+                                      else np.zeros(0, np.int64))
 
     @classmethod
     def concat(cls, logs_list) -> "VisitLogs":
