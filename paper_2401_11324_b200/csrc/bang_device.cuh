@@ -249,6 +249,96 @@ __device__ __forceinline__ bool bloom_resolve(uint32_t *__restrict__ bits, uint3
     return true;
 }
 
+// In-row slot sharing, exact replay by one warp from the pre-state bits the
+// row's probes already loaded -- no L2 round trips (bloom.py:110-122,
+// 134-158).  Inputs (shared memory, probe j = 0..deg-1):
+//   rec[j] = (p1, p2) slots; fl2[2j + h] per half h: bit 1 presumed fresh
+//   (pre-state test), bit 2 pre-state bit of slot h, bit 3 this half's
+//   fetch-or found its bit set by another probe of the row.
+// Every presumed-fresh probe already set its bits with fetch-or.  Only
+// presumed-fresh probes that share a slot can change the sequential outcome
+// (a shared slot always shows up as a collision on one of its fetch-ors), so
+// those "involved" probes are replayed in adjacency order; dropped probes'
+// bits that neither the pre-state nor a truly fresh probe holds are cleared.
+// Output tf[j] = truly fresh (j < RPAD).
+template <int NPL>
+__device__ __forceinline__ int replay_row_warp(const uint2 *rec, const uint8_t *fl2, int deg,
+                                               uint32_t *bits, uint8_t *tf_out) {
+    const int lane = (int)lane_id();
+    uint32_t a[NPL], b[NPL];
+    bool pf[NPL], pre1[NPL], pre2[NPL], inv[NPL], tf[NPL], dr[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+        const int jj = lane + 32 * r;
+        const bool in = jj < deg;
+        const uint2 v = in ? rec[jj] : make_uint2(0u, 0u);
+        const uint8_t f0 = in ? fl2[2 * jj] : 0, f1 = in ? fl2[2 * jj + 1] : 0;
+        a[r] = v.x;
+        b[r] = v.y;
+        pf[r] = (f0 & 2) != 0;
+        pre1[r] = (f0 & 4) != 0;
+        pre2[r] = (f1 & 4) != 0;
+        inv[r] = pf[r] && ((f0 | f1) & 8);
+        tf[r] = dr[r] = false;
+    }
+    // partners: presumed-fresh probes sharing a slot with a colliding one
+#pragma unroll
+    for (int rc = 0; rc < NPL; ++rc) {
+        unsigned cm = __ballot_sync(kFull, inv[rc]);
+        while (cm) {
+            const int src = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const uint32_t pa = __shfl_sync(kFull, a[rc], src), pb = __shfl_sync(kFull, b[rc], src);
+#pragma unroll
+            for (int r = 0; r < NPL; ++r)
+                inv[r] = inv[r] || (pf[r] && (a[r] == pa || a[r] == pb || b[r] == pa || b[r] == pb));
+        }
+    }
+    auto in_set = [&](uint32_t pos) {  // slot set by an earlier truly fresh involved probe
+        bool hit = false;
+#pragma unroll
+        for (int r = 0; r < NPL; ++r) hit = hit || (tf[r] && (a[r] == pos || b[r] == pos));
+        return __any_sync(kFull, hit);
+    };
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+        unsigned im = __ballot_sync(kFull, inv[r]);
+        while (im) {
+            const int src = __ffs(im) - 1;
+            im &= im - 1;
+            const uint32_t pa = __shfl_sync(kFull, a[r], src), pb = __shfl_sync(kFull, b[r], src);
+            const bool q1 = __shfl_sync(kFull, (int)pre1[r], src), q2 = __shfl_sync(kFull, (int)pre2[r], src);
+            const bool h1 = q1 || in_set(pa);
+            const bool h2 = q2 || in_set(pb);
+            if (lane == src) {
+                if (!(h1 && h2)) tf[r] = true;
+                else dr[r] = true;
+            }
+        }
+    }
+    int ndrop = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+        unsigned dm = __ballot_sync(kFull, dr[r]);
+        ndrop += __popc(dm);
+        while (dm) {
+            const int src = __ffs(dm) - 1;
+            dm &= dm - 1;
+            const uint32_t pa = __shfl_sync(kFull, a[r], src), pb = __shfl_sync(kFull, b[r], src);
+            const bool q1 = __shfl_sync(kFull, (int)pre1[r], src), q2 = __shfl_sync(kFull, (int)pre2[r], src);
+            const bool keep_a = q1 || in_set(pa);
+            const bool keep_b = pb == pa || q2 || in_set(pb);
+            if (lane == 0) {
+                if (!keep_a) atomicAnd(bits + (pa >> 5), ~(1u << (pa & 31)));
+                if (!keep_b) atomicAnd(bits + (pb >> 5), ~(1u << (pb & 31)));
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) tf_out[lane + 32 * r] = (uint8_t)(pf[r] && !dr[r]);
+    return ndrop;
+}
+
 // Both phases back to back (the stand-alone bank kernel).
 template <int NPL>
 __device__ __forceinline__ void bloom_test_and_set(uint32_t *__restrict__ bits, uint32_t *s_sum,

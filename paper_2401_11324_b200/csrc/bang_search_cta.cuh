@@ -276,39 +276,16 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
                 const int any_coll = __syncthreads_or(coll);
                 BANG_CTA_PHASE(3)
                 if (any_coll) {
-                    // in-row slot sharing: restore the pre-state, replay in order
-                    if (fresh) {
-                        if (init) __stcg(bits + (ps >> 5), word);
-                        else atomicAnd(s_sum + ((ps >> 5) >> 5), ~(1u << ((ps >> 5) & 31)));
-                    }
-                    if (h == 0 && j < RPAD) s_ids[j] = id;
-                    __threadfence_block();
+                    // in-row slot sharing: exact replay of the involved probes
+                    // by warp 0 from the pre-state bits (replay_row_warp)
+                    uint2 *rec = reinterpret_cast<uint2 *>(s_sk);
+                    uint8_t *fl2 = reinterpret_cast<uint8_t *>(s_nk);
+                    if (h == 0) rec[j].x = ps;
+                    else rec[j].y = ps;
+                    const uint32_t bq = 1u << (ps & 31);
+                    fl2[2 * j + h] = (uint8_t)((fresh ? 2 : 0) | ((word & bq) ? 4 : 0) | (coll ? 8 : 0));
                     __syncthreads();
-                    if (tid == 0) {
-                        for (int q = 0; q < deg; ++q) {
-                            const uint32_t nd = s_ids[q];
-                            const uint32_t q2[2] = {mod_z(fnv1a(nd, kFnvOffset), p.geom),
-                                                    mod_z(fnv1a(nd, kFnvOffsetH2), p.geom)};
-                            bool hit = true;
-                            for (int x = 0; x < 2; ++x) {
-                                const uint32_t w = q2[x] >> 5;
-                                hit = hit && sum_get(s_sum, w) && ((__ldcg(bits + w) >> (q2[x] & 31)) & 1u);
-                            }
-                            s_fl[q] = !hit;
-                            if (!hit) {
-                                for (int x = 0; x < 2; ++x) {
-                                    const uint32_t w = q2[x] >> 5;
-                                    if (!sum_get(s_sum, w)) {
-                                        __stcg(bits + w, 1u << (q2[x] & 31));
-                                        s_sum[w >> 5] |= 1u << (w & 31);
-                                    } else {
-                                        atomicOr(bits + w, 1u << (q2[x] & 31));
-                                    }
-                                }
-                            }
-                        }
-                    }
-                    __threadfence_block();
+                    if (warp == 0) replay_row_warp<RPAD / 32>(rec, fl2, deg, bits, s_fl);
                     __syncthreads();
                     fresh = valid && s_fl[j];
                     continue;  // redo the ADC with the replayed fresh set

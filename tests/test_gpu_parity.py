@@ -348,6 +348,25 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
+@pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z", [
+    (16, 16_000, 96, 64, 48, 64, np.float32, 251),
+    (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
+    (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
+])
+def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z):
+    """Default CTA kernel with small Bloom filters: most rows share slots, so
+    the warp replay from pre-state bits (replay_row_warp) runs constantly."""
+    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=10, t=t, bloom_entries=z, threads=8)
+    res = s.search(q)
+    assert s.last_stats()["kernel"] == 2
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+
+
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
     (14, 16_000, 128, 64, 32, 48, np.uint8),
     (15, 16_000, 96, 64, 48, 64, np.float32),
