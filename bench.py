@@ -444,6 +444,11 @@ def main():
             out["phase_cycles_per_pool_iteration"] = {
                 nm: round(pc[i] / max(1, s_last["iterations"] / max(1, s_last["slots"])) / max(1, s_last["ctas"]), 1)
                 for i, nm in enumerate(names)}
+        elif s_last.get("kernel") == 6:  # search_pf_kernel: thread 32's cycles, slot 1 = warp 0's prefetch
+            names = ["bloom_test", "prefetch_warp0", "adc_reduce", "coll_sync", "survivors_sync", "sort",
+                     "merge_and_final_sync"]
+            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
+            out["phase_cycles_per_iteration"]["prologue_epilogue_per_query"] = round(pc[7] / max(1, nq), 1)
         elif s_last["slots"] == s_last["ctas"]:  # search_cta_kernel: thread 0's cycles
             names = ["bloom_load", "zero_sync", "adc_reduce", "coll_sync", "winner_prefetch", "sort", "merge"]
             out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}

@@ -40,7 +40,7 @@ NO_FAT = 2048
 PIPELINE_ROWS = 4096
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 KERNELS = {0: "search_kernel", 1: "search_tab_kernel", 2: "search_cta_kernel", 3: "search_fat_kernel",
-           4: "search_pool_kernel", 5: "search_ctapipe_kernel"}
+           4: "search_pool_kernel", 5: "search_ctapipe_kernel", 6: "search_pf_kernel"}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

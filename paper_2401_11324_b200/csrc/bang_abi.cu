@@ -22,6 +22,7 @@
 #include "bang_search_pool.cuh"
 #include "bang_search_fat.cuh"
 #include "bang_search_ctapipe.cuh"
+#include "bang_search_pf.cuh"
 
 using namespace bang;
 
@@ -142,6 +143,7 @@ struct Plan {
     bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
     bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
     bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
+    bool pf_kernel = false;   // search_pf_kernel (warp 0 prefetches the next row's Bloom bits)
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
@@ -188,6 +190,17 @@ const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr = false) {
     BANG_C(64, 0, 2) BANG_C(128, 0, 2) BANG_C(256, 0, 2)
     BANG_C(64, 0, 3) BANG_C(128, 0, 3) BANG_C(256, 0, 3)
 #undef BANG_C
+    return nullptr;
+}
+
+const void *pick_pf_kernel(int nt, int sub, int mv) {
+#define BANG_P(N, S, V) \
+    if (nt == N && sub == S && mv == V) return reinterpret_cast<const void *>(&search_pf_kernel<N, S, V>);
+    BANG_P(128, 4, 2) BANG_P(256, 4, 2)
+    BANG_P(128, 2, 3) BANG_P(256, 2, 3)
+    BANG_P(128, 0, 2) BANG_P(256, 0, 2)
+    BANG_P(128, 0, 3) BANG_P(256, 0, 3)
+#undef BANG_P
     return nullptr;
 }
 
@@ -374,11 +387,17 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_tab = take(tab_bytes);
         pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
         pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
+        // one-hop-ahead Bloom/code prefetch by warp 0 (HBM graph; BANG_PF=0 disables)
+        const char *pf = getenv("BANG_PF");
+        pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr && !(pf && *pf == '0') &&
+                       pl.nt >= 128 && t <= 4 * (pl.nt - 32) && pick_pf_kernel(pl.nt, pl.sub, pl.mv);
         if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
         if (pl.fat_kernel) {
             pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
             pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
         }
+        // prefetched slots (u32) + pre-state flags (u8) + warp 0's slot-sharing table
+        if (pl.pf_kernel) pl.off_dup = take(5LL * pl.nt + 4LL * kDupSlots);
         pl.per_warp = off;  // bytes per CTA
         pl.shared_bytes = 0;
         pl.warps = pl.nt / 32;
@@ -386,6 +405,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
         const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                          : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
+                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv)
                                           : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
@@ -487,6 +507,16 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.fat_stride = ix->fat_stride;
     p.fat_code_off = ix->fat_code_off;
     p.off_dup = pl.off_dup;
+    {
+        const char *bc = getenv("BANG_BLOOM_CLEAR");
+        p.bloom_clear = !(bc && *bc == '0');
+        const char *pl2 = getenv("BANG_PF_L2");
+        p.pf_l2 = pl2 ? atoi(pl2) : 2;
+        const char *pr = getenv("BANG_PF_RED");
+        p.pf_red = pr && *pr == '1';
+        const char *ps = getenv("BANG_PF_SPEC");
+        p.pf_spec = !(ps && *ps == '0');
+    }
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -501,6 +531,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     }
     const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv, p.row_hdr != 0)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);
@@ -597,7 +628,7 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
     ix->stats.warps_per_cta = pl.warps;
     ix->stats.ctas = pl.ctas;
     ix->stats.adc_variant = pl.variant;
-    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.pipe_kernel ? 5 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
+    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.pipe_kernel ? 5 : pl.pf_kernel ? 6 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
     ix->last_nq = nq;
     ix->last_log_cap = cap;
     ix->last_has_table = d_table != nullptr;
@@ -1068,10 +1099,14 @@ bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_
     cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : ix->stream;
     const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
     const int sub = ix->uniform_sub;
-    // table + query (+ per-warp double-buffered code-row stages, vector path)
+    // BANG_ADC_PAIRS=lanes: code rows straight into registers, sums carried
+    // across the row's lanes (adc_pairs_lanes_kernel); default: smem-staged rows
+    const char *var = std::getenv("BANG_ADC_PAIRS");
     const bool vec = (sub == 4 && mv == 2) || (sub == 2 && mv == 3);
+    const bool lanes = vec && var && std::strcmp(var, "lanes") == 0;
+    // table + query (+ per-warp double-buffered code-row stages, staged vector path)
     const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + align_up(ix->dim, 4)) +
-                        (vec ? (size_t)8 * 2 * 32 * ix->m : 0);
+                        (vec && !lanes ? (size_t)8 * 2 * 32 * ix->m : 0);
     if (smem > (size_t)ix->max_smem) return fail(BANG_E_PARAM, "table of m=%d does not fit in shared memory", ix->m);
     auto launch = [&](const void *fn) -> bang_status {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1084,6 +1119,8 @@ bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_
         CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st));
         return BANG_OK;
     };
+    if (lanes && sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_lanes_kernel<4, 2>));
+    if (lanes && sub == 2 && mv == 3) return launch(reinterpret_cast<const void *>(&adc_pairs_lanes_kernel<2, 3>));
     if (sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<4, 2>));
     if (sub == 2 && mv == 3) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<2, 3>));
     return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<0, 0>));

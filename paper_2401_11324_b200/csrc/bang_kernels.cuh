@@ -81,6 +81,18 @@ struct SearchParams {
     // read fetches degree + ids (search_cta_kernel stages it at off_row)
     int64_t adj_stride;
     int32_t row_hdr, off_row;
+    // search_cta_kernel: clear the slot's filter with whole-line stores at
+    // query start (else words are zeroed on first touch; BANG_BLOOM_CLEAR=0)
+    int32_t bloom_clear;
+    // search_pf_kernel: L2 prefetch of the next row's code rows (0 none,
+    // 1 cp.async.bulk.prefetch, 2 prefetch.global.L2; BANG_PF_L2)
+    int32_t pf_l2;
+    // search_pf_kernel: fire-and-forget Bloom sets, slot sharing found by
+    // warp 0 ahead of time (BANG_PF_RED=0: fetch-or results)
+    int32_t pf_red;
+    // search_pf_kernel: L2 prefetch of the candidate winners' rows (the head
+    // at expand time, each warp's best fresh neighbour; BANG_PF_SPEC=0 off)
+    int32_t pf_spec;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -891,6 +903,101 @@ __global__ void __launch_bounds__(256) adc_pairs_kernel(const float *__restrict_
             for (int64_t i = lo + tid; i < hi; i += nt) {
                 const uint32_t node = __ldg(ids + i);
                 keys[i] = pack_key(adc_table<0>(s_tab, m, codes + (int64_t)node * m), node);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// -------------------------------------------------------------------------
+// Kernel 3 over query-grouped pairs, lane-pipelined variant: code rows go
+// straight from L2/HBM into registers (no shared-memory staging), MV lanes
+// per row with one coalesced 16-byte load each.  Lane (j, p) owns subspaces
+// [16p, 16p+16) of row j, so the exact sequential f32 sum (engine.py:102-104)
+// is carried across the row's lanes: the partial sum moves one lane up per
+// round (shfl), and lane p works on the batch loaded p rounds before lane 0's.
+// Every lane keeps its own 16-byte piece in a register ring of S = D + MV
+// slots (D = rounds of load lead), so no piece is ever re-read or shuffled.
+// Same arguments and results as adc_pairs_kernel.
+// -------------------------------------------------------------------------
+template <int SUB, int MV>
+__global__ void __launch_bounds__(256, 4) adc_pairs_lanes_kernel(const float *__restrict__ centroids,
+                                                              const int32_t *__restrict__ sub_off,
+                                                              const int32_t *__restrict__ sub_size, int m,
+                                                              int dim, const float *__restrict__ queries,
+                                                              int64_t nq, const int64_t *__restrict__ off,
+                                                              const uint32_t *__restrict__ ids,
+                                                              const uint8_t *__restrict__ codes,
+                                                              uint64_t *__restrict__ keys) {
+    static_assert(SUB == 2 || SUB == 4, "vector path only");
+    constexpr int M = 16 * MV;      // code row bytes
+    constexpr int RPW = 32 / MV;    // rows per warp round
+    constexpr int D = 2;            // load lead, rounds
+    constexpr int S = D + MV;       // register ring slots
+    extern __shared__ __align__(16) float s_tab[];  // m*256 table, then the query
+    float *s_q = s_tab + (size_t)m * 256;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    const int j = lane / MV, p = lane - j * MV;
+    const bool row_lane = j < RPW;
+    const float *tp = s_tab + p * 16 * 256;  // this lane's 16 subspace tables
+    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        for (int i = tid; i < dim; i += nt) s_q[i] = __ldg(queries + q * dim + i);
+        __syncthreads();
+        for (int idx = tid; idx < m * 256; idx += nt) {
+            const int s = idx >> 8, c = idx & 255;
+            float e;
+            if constexpr (SUB == 4)
+                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                                 __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
+            else
+                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                                 __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
+            s_tab[idx] = e;
+        }
+        __syncthreads();
+        const int64_t lo = off[q];
+        const int npair = (int)(off[q + 1] - lo);
+        // this warp's batches b: rows r(b) = warp*RPW + j + b*nw*RPW of the query's pairs
+        const int nbt = (npair + RPW - 1) / RPW;
+        const int nb = nbt > warp ? (nbt - warp + nw - 1) / nw : 0;
+        const int r0w = warp * RPW + j, rstep = nw * RPW;
+        const uint32_t *qids = ids + lo;
+        uint64_t *qkeys = keys + lo;
+        uint4 ring[S];
+        uint32_t rid[S];
+        auto load = [&](int b, uint4 &cv, uint32_t &id) {
+            const int ri = r0w + b * rstep;
+            if (row_lane && b < nb && ri < npair) {
+                id = __ldg(qids + ri);
+                cv = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)id * M) + p);
+            }
+        };
+#pragma unroll
+        for (int u = 0; u < D; ++u) load(u, ring[u], rid[u]);
+        float acc_in = 0.0f;
+        const int nround = nb + MV - 1;
+        for (int r0 = 0; r0 < nround; r0 += S) {
+#pragma unroll
+            for (int u = 0; u < S; ++u) {
+                const int r = r0 + u;
+                if (r >= nround) break;
+                load(r + D, ring[(u + D) % S], rid[(u + D) % S]);
+                // lane p works on batch r - p, whose piece sits in slot (u - p) mod S
+                uint4 cv = ring[u % S];
+                if constexpr (MV >= 2) if (p == 1) cv = ring[(u + S - 1) % S];
+                if constexpr (MV >= 3) if (p == 2) cv = ring[(u + S - 2) % S];
+                const int b = r - p, ri = r0w + b * rstep;
+                const bool live = row_lane && b >= 0 && b < nb && ri < npair;
+                float acc = p == 0 ? 0.0f : acc_in;
+                if (live) {
+                    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        acc = __fadd_rn(acc, tp[i * 256 + ((w[i >> 2] >> ((i & 3) * 8)) & 0xFFu)]);
+                    if (p == MV - 1) qkeys[ri] = pack_key(acc, rid[(u + S - (MV - 1)) % S]);
+                }
+                acc_in = __shfl_up_sync(kFull, acc, 1);
             }
         }
         __syncthreads();

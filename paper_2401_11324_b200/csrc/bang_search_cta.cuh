@@ -21,6 +21,26 @@
 
 namespace bang {
 
+// in-row slot-sharing table (open addressing over Bloom slot numbers), used
+// by search_fat_kernel and search_pf_kernel
+constexpr uint32_t kDupEmpty = 0xFFFFFFFFu;
+constexpr int kDupSlots = 256;
+
+// Claims slot ps in the row's table; true if another probe of the row already
+// holds it.  *didx = the entry this probe filled (cleared after the row).
+__device__ __forceinline__ bool dup_claim(uint32_t *s_dup, uint32_t ps, int *didx) {
+    uint32_t x = (ps * 0x9E3779B1u) >> 24;
+    for (;;) {
+        const uint32_t old = atomicCAS(s_dup + x, kDupEmpty, ps);
+        if (old == kDupEmpty) {
+            *didx = (int)x;
+            return false;
+        }
+        if (old == ps) return true;
+        x = (x + 1) & (kDupSlots - 1);
+    }
+}
+
 struct CtaMisc {
     unsigned long long wmin[8];  // per-warp survivor minimum
     int wcnt[8];                 // per-warp survivor count
@@ -116,6 +136,14 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
         for (int i = tid; i < p.dim; i += NT) s_q[i] = __ldg(p.queries + qid * p.dim + i);
         for (int i = tid; i < p.sum_words; i += NT) s_sum[i] = 0u;
         for (int i = tid; i < t; i += NT) s_vis[i] = 0;
+        if (p.bloom_clear) {
+            // the filter starts empty: whole-sector stores keep its lines
+            // complete in L2, so the fetch-or atomics and word loads of this
+            // query hit L2 instead of filling partially written sectors
+            uint4 *b4 = reinterpret_cast<uint4 *>(bits);
+            const int n4 = (int)(p.bloom_stride >> 2);
+            for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
+        }
         __syncthreads();
         // kernel 1 for this query into shared memory (pq.py:284-296)
         for (int idx = tid; idx < M * 256; idx += NT) {
@@ -220,7 +248,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             // words first written by this query: zero + summary, then (after
             // the barrier) the fetch-or atomics
             if (fresh && !init) {
-                __stcg(bits + (ps >> 5), 0u);
+                if (!p.bloom_clear) __stcg(bits + (ps >> 5), 0u);
                 sum_set(s_sum, ps >> 5);
             }
             __syncthreads();  // zeroing stores (any warp) before any atomic; publishes head

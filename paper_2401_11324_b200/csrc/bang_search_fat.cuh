@@ -32,8 +32,6 @@
 
 namespace bang {
 
-constexpr uint32_t kDupEmpty = 0xFFFFFFFFu;
-constexpr int kDupSlots = 256;
 
 // One warp per node: ids, then the code rows of its neighbours (m = 16*MV).
 __global__ void build_fat_rows_kernel(const int32_t *__restrict__ adj, const int32_t *__restrict__ deg,

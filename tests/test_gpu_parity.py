@@ -7,6 +7,8 @@ arithmetic order is restated), with the stated tolerance 1e-4 relative only
 used where noted.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -117,10 +119,13 @@ def test_kernel3_adc_vectorised_code_rows():
             assert np.array_equal(got, want[rows == q])
 
 
+@pytest.mark.parametrize("variant", ["staged", "lanes"])
 @pytest.mark.parametrize("d,m", [(128, 32), (96, 48), (20, 8)])
-def test_kernel3_adc_pairs_query_grouped(d, m):
+def test_kernel3_adc_pairs_query_grouped(d, m, variant, monkeypatch):
     """bang_adc_pairs_device (table built in shared memory per query) equals
-    the oracle's table + sequential ADC, including empty pair ranges."""
+    the oracle's table + sequential ADC, including empty pair ranges; both
+    code-row data flows (smem-staged rows, lane-pipelined register rows)."""
+    monkeypatch.setenv("BANG_ADC_PAIRS", variant)
     import torch
     from paper_2401_11324_b200 import _lib
     from paper_2401_11324_b200.tools.pq_train import encode, train_codebook
@@ -342,9 +347,18 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     if m in (32, 48) and R <= 64:
         variants.append("pool")
         s.set_adc_variant("auto").search(q[:4])
-        assert s.last_stats()["kernel"] == 2  # CTA per query with the smem table
+        # CTA per query with the smem table; R > 32: warp 0 prefetches the next row
+        assert s.last_stats()["kernel"] == (6 if R > 32 else 2)
     for variant in variants:
         res = s.set_adc_variant(variant).search(q)
+        _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    if m in (32, 48) and R > 32:
+        os.environ["BANG_PF"] = "0"  # the CTA kernel without the prefetching warp
+        try:
+            res = s.set_adc_variant("auto").search(q)
+            assert s.last_stats()["kernel"] == 2
+        finally:
+            del os.environ["BANG_PF"]
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
@@ -353,9 +367,15 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z):
+@pytest.mark.parametrize("pf", ["1", "0", "red"])
+def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, pf, monkeypatch):
     """Default CTA kernel with small Bloom filters: most rows share slots, so
-    the warp replay from pre-state bits (replay_row_warp) runs constantly."""
+    the warp replay from pre-state bits (replay_row_warp) runs constantly.
+    pf=1: the prefetching variant (search_pf_kernel, in-row slot sharing
+    from fetch-or results); red: search_pf_kernel with sharing found ahead by
+    warp 0 and fire-and-forget sets; 0: search_cta_kernel."""
+    monkeypatch.setenv("BANG_PF", "0" if pf == "0" else "1")
+    monkeypatch.setenv("BANG_PF_RED", "1" if pf == "red" else "0")
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
@@ -363,7 +383,7 @@ def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z):
                     adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
                     k=10, t=t, bloom_entries=z, threads=8)
     res = s.search(q)
-    assert s.last_stats()["kernel"] == 2
+    assert s.last_stats()["kernel"] == (2 if pf == "0" else 6)
     _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
 
 
