@@ -108,6 +108,7 @@ struct bang_index {
     int sm_count = 148;
     int max_smem = 227 * 1024;
     int64_t persist_max = 0, window_max = 0;  // L2 persistence limits of the device
+    int64_t l2_bytes = 0;                      // L2 capacity of the device
     size_t persist_set = 0;
     // workspace
     DevBuf<float> q, table;
@@ -387,9 +388,14 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_tab = take(tab_bytes);
         pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
         pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
-        // one-hop-ahead Bloom/code prefetch by warp 0 (HBM graph; BANG_PF=0 disables)
+        // one-hop-ahead Bloom/code prefetch by warp 0 (graph in HBM).  It pays
+        // when the next row's loads miss L2 -- codes larger than L2 (C3: 480 MB,
+        // +5-9%); with L2-resident codes (C2: 32 MB) the serial prefetch warp
+        // costs more than it hides (-13%).  BANG_PF=1/0 forces it on/off.
         const char *pf = getenv("BANG_PF");
-        pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr && !(pf && *pf == '0') &&
+        const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
+        pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr &&
+                       (pf ? *pf == '1' : pf_auto) &&
                        pl.nt >= 128 && t <= 4 * (pl.nt - 32) && pick_pf_kernel(pl.nt, pl.sub, pl.mv);
         if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
         if (pl.fat_kernel) {
@@ -516,6 +522,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
         p.pf_red = pr && *pr == '1';
         const char *ps = getenv("BANG_PF_SPEC");
         p.pf_spec = !(ps && *ps == '0');
+        const char *pe = getenv("BANG_PF_EAGER");
+        p.pf_eager = pe && *pe == '1';
     }
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
@@ -744,6 +752,7 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
     ix->sm_count = prop.multiProcessorCount;
     ix->max_smem = (int)prop.sharedMemPerBlockOptin;
     ix->persist_max = prop.persistingL2CacheMaxSize;
+    ix->l2_bytes = prop.l2CacheSize;
     ix->window_max = prop.accessPolicyMaxWindowSize;
     CUX(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) CUX(cudaEventCreate(&e));

@@ -93,6 +93,7 @@ struct SearchParams {
     // search_pf_kernel: L2 prefetch of the candidate winners' rows (the head
     // at expand time, each warp's best fresh neighbour; BANG_PF_SPEC=0 off)
     int32_t pf_spec;
+    int32_t pf_eager;  // (measurement only) wait for the fetch-or before the ADC
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

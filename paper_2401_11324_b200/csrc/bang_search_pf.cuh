@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 if (p.pf_red) atomicOr(bits + (ps >> 5), 1u << (ps & 31));
                 else old = atomicOr(bits + (ps >> 5), 1u << (ps & 31));
             }
-            const bool shared = p.pf_red ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0;
+            if (p.pf_eager) asm volatile("" ::"r"(old));  // A/B: wait for the fetch-or here
             const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
             uint64_t key = kSentinel;
             bool surv = false;
@@ -347,7 +347,9 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 const unsigned sb = __ballot_sync(kFull, surv);
                 const unsigned fb = __ballot_sync(kFull, fresh && h == 1);
                 // Bloom collision check (fetch-or results) folded into the barrier
-                const bool coll = pass == 0 && do_atom && shared && !mybit;
+                // (the fetch-or result is consumed only here, after the ADC)
+                const bool coll = pass == 0 && do_atom && !mybit &&
+                                  (p.pf_red ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0);
                 if (lane == 0) {
                     s_m->wmin[warp] = wm;
                     s_m->wcnt[warp] = __popc(sb);

@@ -347,16 +347,15 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     if m in (32, 48) and R <= 64:
         variants.append("pool")
         s.set_adc_variant("auto").search(q[:4])
-        # CTA per query with the smem table; R > 32: warp 0 prefetches the next row
-        assert s.last_stats()["kernel"] == (6 if R > 32 else 2)
+        assert s.last_stats()["kernel"] == 2  # CTA per query with the smem table (codes fit L2)
     for variant in variants:
         res = s.set_adc_variant(variant).search(q)
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
     if m in (32, 48) and R > 32:
-        os.environ["BANG_PF"] = "0"  # the CTA kernel without the prefetching warp
+        os.environ["BANG_PF"] = "1"  # warp 0 prefetches the next row (default when codes exceed L2)
         try:
             res = s.set_adc_variant("auto").search(q)
-            assert s.last_stats()["kernel"] == 2
+            assert s.last_stats()["kernel"] == 6
         finally:
             del os.environ["BANG_PF"]
         _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
