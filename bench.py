@@ -274,8 +274,12 @@ def main():
                         if thr_only else
                         "GPU kNN(2R) + RobustPrune(1.2) + reverse edges (tools/graph_build.py)"
                         if meta["n"] <= EXACT_KNN_LIMIT else
-                        "GPU IVF kNN(2R) + RobustPrune(1.2) + reverse edges, then one search-based Vamana "
-                        "pass (t=64) with this search (tools/graph_build.py)"),
+                        "GPU IVF kNN(2R) + RobustPrune(1.2) + reverse edges, then search-based Vamana "
+                        "passes (t=128, 128, 200) with this search (tools/graph_build.py)"),
+              "layout": ("random node order" if thr_only else
+                         "node ids in k-means partition order (index relabelled at build so graph neighbours "
+                         "are near in memory; graph_build.locality_order)" if meta.get("layout") == "partition"
+                         else "generator order"),
               "l2": "flushed between steps (256 MiB memset outside the step events)",
               "parallelism": f"query-sharded x{world}, index replicated, no collective"}
 

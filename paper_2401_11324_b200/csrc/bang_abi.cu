@@ -495,6 +495,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.rerank = (flags & BANG_RERANK) ? 1 : 0;
     p.debug = (flags & BANG_DEBUG_CHECKS) ? 1 : 0;
     p.profile = (flags & BANG_PROFILE_PHASES) ? 1 : 0;
+    if (p.profile && getenv("BANG_PF_BREAKDOWN")) p.profile = 2;  // pf kernel: slots 4/5 = warp 0's stages
     p.smem_shared_bytes = pl.shared_bytes;
     p.per_warp_bytes = pl.per_warp;
     p.off_q = pl.off_q;

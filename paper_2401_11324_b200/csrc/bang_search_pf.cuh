@@ -77,12 +77,19 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
                                        uint8_t *s_nfl, uint32_t *s_dup, PfMisc *s_m) {
     constexpr int PL = NT / 64;  // neighbour slots per lane (RPAD = NT/2)
     constexpr int M = 16 * MV;
+    const long long c0 = p.profile == 2 ? clock64() : 0;
     const int deg = p.deg[w];
     uint32_t nid[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
         const int jj = lane + 32 * r;
         nid[r] = jj < p.R ? (uint32_t)p.adj[(int64_t)w * p.adj_stride + jj] : 0u;
+    }
+    if (p.profile == 2 && lane == 0) {  // (breakdown) row arrival
+        uint32_t x = nid[0];
+#pragma unroll
+        for (int r = 1; r < PL; ++r) x ^= nid[r];
+        s_m->ph[4] += (unsigned long long)(clock_after((int)x + deg) - c0);
     }
     uint32_t ps1[PL], ps2[PL], wd1[PL], wd2[PL];
     bool i1[PL], i2[PL];
@@ -106,6 +113,12 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
             if (i1[r]) wd1[r] = __ldcg(bits + (ps1[r] >> 5));
             if (i2[r]) wd2[r] = __ldcg(bits + (ps2[r] >> 5));
         }
+    }
+    if (p.profile == 2 && lane == 0) {  // (breakdown) hashes + Bloom word arrival
+        uint32_t x = 0;
+#pragma unroll
+        for (int r = 0; r < PL; ++r) x ^= wd1[r] ^ wd2[r];
+        s_m->ph[5] += (unsigned long long)(clock_after((int)x) - c0);
     }
     // slot sharing among the row's probes (exact, open addressing): the later
     // claimer of a shared slot is flagged; a node's own p1 == p2 is one claim
@@ -402,7 +415,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 if (p.profile && tid == 0) s_m->ph[1] += (unsigned long long)(clock_after(s_nfl[0]) - c0);
             } else {
                 named_bar_sync(1, NT);  // all survivors published
-                BANG_PF_PHASE(4)
+                if (p.profile == 2) s_m->t_ph = clock64(); else { BANG_PF_PHASE(4) }
                 // ---- kernel 4a: rank sort of the survivors
                 for (int q = tc; q < n; q += NC) {
                     const uint64_t k = s_nk[q];
@@ -413,7 +426,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                     s_sk[r] = k;
                 }
                 named_bar_sync(2, NC);
-                BANG_PF_PHASE(5)
+                if (p.profile == 2) s_m->t_ph = clock64(); else { BANG_PF_PHASE(5) }
                 // ---- kernel 4b: merge + truncate to t (engine.py:210-215)
                 if (tc == 0) {
                     int wpos = t;

@@ -50,6 +50,12 @@ EXACT_KNN_LIMIT = 2_000_000
 # from 0.846 to 0.911, a third at t=200 to 0.918 (0.897 at t=160)
 # (profiles/r01/c3_graph_study*.jsonl).
 REFINE = (128, 128, 200)
+# Index layout of the real-graph configs: "partition" relabels the built index
+# so graph neighbours are near in memory (graph_build.locality_order);
+# "natural" (default) keeps the generator's order.  Measured at C3: no QPS
+# difference (720K vs 726K, profiles/r01/layout_C3.txt) -- the search is bound
+# by per-iteration latency, not by DRAM pages.  BANG_BENCH_LAYOUT overrides.
+LAYOUT = os.environ.get("BANG_BENCH_LAYOUT", "natural")
 
 
 def refine_with_search(base, graph, codebook, codes, R, t=64, sigma=1.2, chunk=1 << 20, log=print):
@@ -117,7 +123,7 @@ def build_random_artifacts(name: str, seed: int = 0, nq_total: int | None = None
 
 
 def _key(name, seed, nq_total):
-    return hashlib.sha1(f"v3|{name}|{CONFIGS[name]}|{REFINE}|{seed}|{nq_total}".encode()).hexdigest()[:16]
+    return hashlib.sha1(f"v3|{name}|{CONFIGS[name]}|{REFINE}|{seed}|{nq_total}|{LAYOUT}".encode()).hexdigest()[:16]
 
 
 _ARRAYS = ("base", "queries", "adjacency", "degrees", "medoid", "sub_sizes", "centroids", "codes",
@@ -171,7 +177,7 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         return build_random_artifacts(name, seed, nq_total, log)
     n, nq, dim, dt, clusters, R, m, desc = CONFIGS[name]
     nq_total = nq_total or nq
-    meta = dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters)
+    meta = dict(desc=desc, n=n, dim=dim, dtype=dt, R=R, m=m, clusters=clusters, layout=LAYOUT)
     path = None
     if cache_dir:
         os.makedirs(cache_dir, exist_ok=True)
@@ -196,6 +202,13 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
             graph = refine_with_search(base, graph, cb, codes, R, t=t_ref, log=log)
         t2 += time.time() - t3
         t3 = time.time()
+    if LAYOUT == "partition":
+        from .graph_build import locality_order, relabel_index
+        perm = locality_order(base, seed=seed)
+        base, adj, deg, med = relabel_index(perm, base, graph.adjacency, graph.degrees, graph.medoid)
+        graph = GraphIndex(adj, deg, med, R, validate=False)
+        codes = CompressedVectors(np.ascontiguousarray(codes.codes[perm]))
+        log(f"[bench_data] {name}: relabelled in k-means partition order ({time.time() - t3:.1f}s)")
     gt_ids, gt_d = brute_force_knn(base, queries, 10)
     t4 = time.time()
     log(f"[bench_data] {name}: data {t1 - t0:.1f}s graph {t2 - t1:.1f}s pq {t3 - t2:.1f}s gt {t4 - t3:.1f}s"

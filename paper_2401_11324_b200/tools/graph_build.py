@@ -233,6 +233,61 @@ def knn_ivf(x, K: int, nlist: int = 0, nprobe: int = 8, max_rows: int = 4096, se
     return out_i, out_d
 
 
+def locality_order(base, nlist: int = 0, seed: int = 0, device=None) -> np.ndarray:
+    """Index layout: a node order in which graph neighbours sit close in
+    memory.  k-means cells (about 1,000 points each) are chained greedily by
+    nearest centroid, and nodes are laid out cell by cell, so the code rows,
+    adjacency rows and vectors a search gathers for one region of space share
+    L2 lines and DRAM pages.  Returns perm: new position -> old id.  Applying
+    it (relabel_index) renames nodes only; the graph and the search over it
+    are unchanged."""
+    import torch
+    dev = device if device is not None else torch_device()
+    xn = np.asarray(base)
+    n = xn.shape[0]
+    nlist = nlist or max(1, n // 1000)
+    x = torch.from_numpy(np.ascontiguousarray(xn)).to(dev)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        cent = kmeans(x, nlist, seed=seed)
+        assign = torch.empty(n, dtype=torch.int64, device=dev)
+        for lo in range(0, n, 1 << 21):
+            assign[lo:lo + (1 << 21)] = _nearest_centroids(x[lo:lo + (1 << 21)].float(), cent, 1)[:, 0]
+        # greedy nearest-neighbour chain through the centroids
+        csq = cent.square().sum(1)
+        d = csq[:, None] + csq[None, :] - 2.0 * (cent @ cent.T)
+        used = torch.zeros(nlist, dtype=torch.bool, device=dev)
+        rank = torch.empty(nlist, dtype=torch.int64, device=dev)
+        cur = int(torch.argmin(csq))
+        for r in range(nlist):
+            rank[cur] = r
+            used[cur] = True
+            if r + 1 < nlist:
+                cur = int(torch.argmin(torch.where(used, float("inf"), d[cur])))
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    key = rank[assign] * n + torch.arange(n, device=dev)
+    return torch.argsort(key).cpu().numpy()
+
+
+def relabel_index(perm: np.ndarray, base, adjacency, degrees, medoid: int, device=None):
+    """Nodes renamed by perm (new position -> old id): returns (base, adjacency,
+    degrees, medoid) in the new order; adjacency entries are renamed, -1
+    padding kept."""
+    import torch
+    dev = device if device is not None else torch_device()
+    n = perm.shape[0]
+    p = torch.from_numpy(perm).to(dev)
+    inv = torch.empty(n, dtype=torch.int32, device=dev)
+    inv[p] = torch.arange(n, dtype=torch.int32, device=dev)
+    adj = torch.from_numpy(np.ascontiguousarray(adjacency)).to(dev)[p]
+    adj = torch.where(adj >= 0, inv[adj.clamp_min(0).long()], adj)
+    deg = np.ascontiguousarray(np.asarray(degrees)[perm])
+    out_base = np.ascontiguousarray(np.asarray(base)[perm])
+    return out_base, adj.cpu().numpy(), deg, int(inv[int(medoid)])
+
+
 def medoid_of(x, chunk: int = 1 << 21) -> int:
     """compute_medoid (graph.py:107-115) on the device: f64 mean, f64 distances."""
     import torch
