@@ -145,6 +145,7 @@ struct Plan {
     bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
     bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
     bool pf_kernel = false;   // search_pf_kernel (warp 0 prefetches the next row's Bloom bits)
+    int pfw = 1;              // search_pf_kernel: prefetch warps
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
@@ -194,9 +195,11 @@ const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr = false) {
     return nullptr;
 }
 
-const void *pick_pf_kernel(int nt, int sub, int mv) {
-#define BANG_P(N, S, V) \
-    if (nt == N && sub == S && mv == V) return reinterpret_cast<const void *>(&search_pf_kernel<N, S, V>);
+const void *pick_pf_kernel(int nt, int sub, int mv, int pfw = 1) {
+#define BANG_P(N, S, V)                                                                            \
+    if (nt == N && sub == S && mv == V)                                                            \
+        return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2>)            \
+                        : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1>);
     BANG_P(128, 4, 2) BANG_P(256, 4, 2)
     BANG_P(128, 2, 3) BANG_P(256, 2, 3)
     BANG_P(128, 0, 2) BANG_P(256, 0, 2)
@@ -394,9 +397,14 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         // costs more than it hides (-13%).  BANG_PF=1/0 forces it on/off.
         const char *pf = getenv("BANG_PF");
         const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
+        // prefetch warps: two halve the per-lane hashing of the next row (C3:
+        // 765K vs 739K QPS) while two warps still cover sort + merge at
+        // t <= 4*(nt-64); BANG_PF_WARPS=1/2 forces the count
+        const char *pfw = getenv("BANG_PF_WARPS");
+        pl.pfw = pfw ? (*pfw == '2' ? 2 : 1) : (t <= 4 * (pl.nt - 64) ? 2 : 1);
         pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr &&
                        (pf ? *pf == '1' : pf_auto) &&
-                       pl.nt >= 128 && t <= 4 * (pl.nt - 32) && pick_pf_kernel(pl.nt, pl.sub, pl.mv);
+                       pl.nt >= 128 && t <= 4 * (pl.nt - 32 * pl.pfw) && pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw);
         if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
         if (pl.fat_kernel) {
             pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
@@ -411,7 +419,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
         const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                          : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv)
+                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw)
                                           : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
@@ -540,7 +548,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     }
     const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv)
+                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw)
                       : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv, p.row_hdr != 0)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);

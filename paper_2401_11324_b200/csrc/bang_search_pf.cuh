@@ -71,18 +71,19 @@ __device__ __forceinline__ long long clock_after(int v) {
 // Warp 0: the row of node w -> s_nid (ids), s_nps (slot per probe half),
 // s_nfl (bit0 = pre-state bit, bit1 = word marked in the summary), ndeg; the
 // code rows are prefetched into L2.
-template <int NT, int MV>
+template <int NT, int MV, int PFW>
 __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int lane, const uint32_t *s_sum,
                                        const uint32_t *bits, uint32_t *s_nid, uint32_t *s_nps,
                                        uint8_t *s_nfl, uint32_t *s_dup, PfMisc *s_m) {
-    constexpr int PL = NT / 64;  // neighbour slots per lane (RPAD = NT/2)
+    constexpr int PL = NT / (64 * PFW);  // neighbour slots per lane (RPAD = NT/2 over PFW warps)
+    constexpr int PT = 32 * PFW;         // prefetch threads; lane = index among them
     constexpr int M = 16 * MV;
     const long long c0 = p.profile == 2 ? clock64() : 0;
     const int deg = p.deg[w];
     uint32_t nid[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
-        const int jj = lane + 32 * r;
+        const int jj = lane + PT * r;
         nid[r] = jj < p.R ? (uint32_t)p.adj[(int64_t)w * p.adj_stride + jj] : 0u;
     }
     if (p.profile == 2 && lane == 0) {  // (breakdown) row arrival
@@ -95,7 +96,7 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     bool i1[PL], i2[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
-        const int jj = lane + 32 * r;
+        const int jj = lane + PT * r;
         ps1[r] = ps2[r] = wd1[r] = wd2[r] = 0u;
         i1[r] = i2[r] = false;
         if (jj < deg) {
@@ -128,12 +129,13 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     for (int r = 0; r < PL; ++r) {
         sh1[r] = sh2[r] = false;
         d1[r] = d2[r] = -1;
-        if (p.pf_red && lane + 32 * r < deg) {
+        if (p.pf_red && lane + PT * r < deg) {
             sh1[r] = dup_claim(s_dup, ps1[r], &d1[r]);
             if (ps2[r] != ps1[r]) sh2[r] = dup_claim(s_dup, ps2[r], &d2[r]);
         }
     }
-    __syncwarp();
+    if (PFW == 1) __syncwarp();
+    else named_bar_sync(3, PT);
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
         if (d1[r] >= 0) s_dup[d1[r]] = kDupEmpty;
@@ -141,7 +143,7 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     }
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
-        const int jj = lane + 32 * r;
+        const int jj = lane + PT * r;
         s_nid[jj] = nid[r];
         s_nps[2 * jj] = ps1[r];
         s_nps[2 * jj + 1] = ps2[r];
@@ -151,10 +153,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     if (lane == 0) s_m->ndeg = deg;
 }
 
-template <int NT, int SUB, int MV>
+template <int NT, int SUB, int MV, int PFW>
 __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kernel(const SearchParams p) {
     constexpr int NW = NT / 32;
-    constexpr int NC = NT - 32;     // sort/merge threads (warps 1..)
+    constexpr int NC = NT - 32 * PFW;  // sort/merge threads (warps PFW..)
     constexpr int M = 16 * MV;
     constexpr int MH = M / 2;       // subspaces per half
     constexpr int MHW = MH / 4;     // code words (u32) per half
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     extern __shared__ __align__(16) unsigned char smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j = tid >> 1, h = tid & 1;
-    const int tc = tid - 32;  // index among the sort/merge threads
+    const int tc = tid - 32 * PFW;  // index among the sort/merge threads
+    const bool pfw = warp < PFW;    // a prefetch warp
     const unsigned lt = (1u << lane) - 1u;
 
     float *s_q = reinterpret_cast<float *>(smem + p.off_q);
@@ -186,8 +189,8 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     unsigned long long st_iters = 0, st_probes = 0, st_fresh = 0, st_rr = 0;
     // phase profiler: thread 32 (a sort/merge thread) per phase; slot 1 =
     // thread 0's cycles in the one-hop-ahead prefetch
-    const bool prof = p.profile && tid == 32;
-    if (tid == 32)
+    const bool prof = p.profile && tc == 0;
+    if (tc == 0)
         for (int i = 0; i < 8; ++i) s_m->ph[i] = 0;
     for (int i = tid; i < kDupSlots; i += NT) s_dup[i] = kDupEmpty;  // (barrier at the query fetch)
 #define BANG_PF_PHASE(i)                                       \
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
             s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
         }
-        if (warp == 0) pf_row<NT, MV>(p, (uint32_t)p.medoid, lane, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+        if (pfw) pf_row<NT, MV, PFW>(p, (uint32_t)p.medoid, tid, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
@@ -407,11 +410,11 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             // ---- survivors -> s_nk (warp-aggregated)
             const unsigned sball = __ballot_sync(kFull, surv);
             if (surv) s_nk[woff + __popc(sball & lt)] = key;
-            if (warp == 0) {
-                // ---- one hop ahead: the winner's row while warps 1.. sort + merge
+            if (pfw) {
+                // ---- one hop ahead: the winner's row while warps PFW.. sort + merge
                 named_bar_arrive(1, NT);
                 const long long c0 = p.profile ? clock64() : 0;
-                if (winner != kSentinel) pf_row<NT, MV>(p, wid, lane, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+                if (winner != kSentinel) pf_row<NT, MV, PFW>(p, wid, tid, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
                 if (p.profile && tid == 0) s_m->ph[1] += (unsigned long long)(clock_after(s_nfl[0]) - c0);
             } else {
                 named_bar_sync(1, NT);  // all survivors published
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         BANG_PF_PHASE(7)
     }
 #undef BANG_PF_PHASE
-    if (p.profile && tid == 32) {
+    if (p.profile && tc == 0) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) atomicAdd(p.counters + kCtrPhase0 + i, s_m->ph[i]);
     }
@@ -551,7 +554,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         atomicAdd(p.counters + kCtrIterations, st_iters);
         atomicAdd(p.counters + kCtrRerank, st_rr);
     }
-    if (tid == 32) {
+    if (tc == 0) {
         // probes/fresh were accumulated uniformly by every thread: count once per CTA
         atomicAdd(p.counters + kCtrProbes, st_probes);
         atomicAdd(p.counters + kCtrFresh, st_fresh);
