@@ -3,13 +3,14 @@ travels with the repository snapshot to the GPU box)."""
 
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = [os.path.join(HERE, "csrc", "bang_abi.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("bang_device.cuh", "bang_kernels.cuh", "bang_search_tab.cuh", "bang_search_cta.cuh", "bang_search_pool.cuh", "bang_search_fat.cuh", "bang_search_ctapipe.cuh")] + \
+DEPS = SRC + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + \
     [os.path.join(os.path.dirname(HERE), "include", "bang.h")]
 OUT = os.path.join(HERE, "libbang.so")
 

@@ -109,6 +109,7 @@ struct bang_index {
     int max_smem = 227 * 1024;
     int64_t persist_max = 0, window_max = 0;  // L2 persistence limits of the device
     int64_t l2_bytes = 0;                      // L2 capacity of the device
+    int64_t smem_per_sm = 0;                   // shared memory per SM
     size_t persist_set = 0;
     // workspace
     DevBuf<float> q, table;
@@ -146,6 +147,9 @@ struct Plan {
     bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
     bool pf_kernel = false;   // search_pf_kernel (warp 0 prefetches the next row's Bloom bits)
     int pfw = 1;              // search_pf_kernel: prefetch warps
+    bool pf_red = false;      // search_pf_kernel: fire-and-forget sets
+    bool pf_stage = false;    // search_pf_kernel: next row's code rows staged in smem
+    int off_code = 0;
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
     int pool_slots = 0, rr_ctas = 0;
@@ -379,22 +383,12 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.nt = 2 * rpad;
         int off = 0;
         auto take = [&](int64_t bytes) { const int o = off; off += (int)align_up(bytes, 16); return o; };
-        pl.off_q = take(4LL * ix->dim);
-        pl.off_wl = take(8LL * t);
-        pl.off_sk = take(8LL * rpad);
-        pl.off_nk = take(8LL * rpad);
-        pl.off_fid = take(4LL * rpad);
-        pl.off_alive = take(rpad);
-        pl.off_acc = take(256);  // CtaMisc
-        pl.off_vis = take(t);
-        pl.off_sum = take(4LL * pl.sum_words);
-        pl.off_tab = take(tab_bytes);
         pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
         pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
-        // one-hop-ahead Bloom/code prefetch by warp 0 (graph in HBM).  It pays
-        // when the next row's loads miss L2 -- codes larger than L2 (C3: 480 MB,
-        // +5-9%); with L2-resident codes (C2: 32 MB) the serial prefetch warp
-        // costs more than it hides (-13%).  BANG_PF=1/0 forces it on/off.
+        // one-hop-ahead prefetch of the next row by dedicated warps (graph in
+        // HBM).  It pays when the next row's loads miss L2 -- codes larger than
+        // L2 (C3: 480 MB); with L2-resident codes (C2: 32 MB) the prefetch warps
+        // cost more than they hide (-13%).  BANG_PF=1/0 forces it on/off.
         const char *pf = getenv("BANG_PF");
         const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
         // prefetch warps: two halve the per-lane hashing of the next row (C3:
@@ -405,13 +399,37 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr &&
                        (pf ? *pf == '1' : pf_auto) &&
                        pl.nt >= 128 && t <= 4 * (pl.nt - 32 * pl.pfw) && pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw);
+        const char *pr = getenv("BANG_PF_RED");
+        pl.pf_red = pl.pf_kernel && pr && *pr == '1';
+        pl.off_q = take(4LL * ix->dim);
+        pl.off_wl = take(8LL * t);
+        pl.off_sk = take(8LL * rpad);
+        pl.off_nk = take(8LL * rpad);
+        pl.off_fid = take(4LL * rpad);
+        pl.off_alive = take(rpad);
+        pl.off_acc = take(256);  // CtaMisc
+        pl.off_vis = take(t);
+        // search_pf_kernel clears its filter per query and reads every probe's
+        // word: no summary (its 1.5 KB hold the staged code rows instead)
+        pl.off_sum = pl.pf_kernel ? 0 : take(4LL * pl.sum_words);
+        pl.off_tab = take(tab_bytes);
         if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
         if (pl.fat_kernel) {
             pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
             pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
         }
-        // prefetched slots (u32) + pre-state flags (u8) + warp 0's slot-sharing table
-        if (pl.pf_kernel) pl.off_dup = take(5LL * pl.nt + 4LL * kDupSlots);
+        if (pl.pf_kernel) {
+            // prefetched slots (u32) + pre-state flags (u8) [+ slot-sharing table]
+            pl.off_dup = take(5LL * pl.nt + (pl.pf_red ? 4LL * kDupSlots : 0));
+            // the next row's code rows, staged by the prefetch warps when they fit
+            const int64_t code_bytes = (int64_t)rpad * 16 * pl.mv;
+            const char *st = getenv("BANG_PF_STAGE");
+            // (the residency search_pf_kernel's launch bounds target: 4 CTAs of
+            // 128 threads at m = 48, 6 at m = 32)
+            const int64_t budget = (int64_t)ix->smem_per_sm / std::max(1, (pl.mv == 3 ? 512 : 768) / pl.nt) - 1024;
+            pl.pf_stage = !(st && *st == '0') && pl.mv > 0 && off + align_up(code_bytes, 16) <= budget;
+            if (pl.pf_stage) pl.off_code = take(code_bytes);
+        }
         pl.per_warp = off;  // bytes per CTA
         pl.shared_bytes = 0;
         pl.warps = pl.nt / 32;
@@ -527,8 +545,9 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
         p.bloom_clear = !(bc && *bc == '0');
         const char *pl2 = getenv("BANG_PF_L2");
         p.pf_l2 = pl2 ? atoi(pl2) : 2;
-        const char *pr = getenv("BANG_PF_RED");
-        p.pf_red = pr && *pr == '1';
+        p.pf_red = pl.pf_red;
+        p.pf_stage = pl.pf_stage;
+        p.off_code = pl.off_code;
         const char *ps = getenv("BANG_PF_SPEC");
         p.pf_spec = !(ps && *ps == '0');
         const char *pe = getenv("BANG_PF_EAGER");
@@ -762,6 +781,7 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
     ix->max_smem = (int)prop.sharedMemPerBlockOptin;
     ix->persist_max = prop.persistingL2CacheMaxSize;
     ix->l2_bytes = prop.l2CacheSize;
+    ix->smem_per_sm = prop.sharedMemPerMultiprocessor;
     ix->window_max = prop.accessPolicyMaxWindowSize;
     CUX(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) CUX(cudaEventCreate(&e));

@@ -94,6 +94,9 @@ struct SearchParams {
     // at expand time, each warp's best fresh neighbour; BANG_PF_SPEC=0 off)
     int32_t pf_spec;
     int32_t pf_eager;  // (measurement only) wait for the fetch-or before the ADC
+    // search_pf_kernel: the prefetch warps stage the next row's code rows at
+    // off_code (rpad x 16*MV bytes) instead of prefetching them into L2
+    int32_t pf_stage, off_code;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

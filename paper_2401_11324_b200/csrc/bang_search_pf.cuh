@@ -2,22 +2,24 @@
 // taken off the critical path (the paper's "one hop ahead" prefetch,
 // PAPER.md:922-938, carried to the Bloom words and code rows).
 //
-// As soon as the eager winner is known (engine.py:201-205) warp 0 leaves the
-// iteration's sort + merge to warps 1.. and, for the winner's adjacency row,
-//   * loads the neighbour ids and the degree,
-//   * hashes every id into its two Bloom slots (bloom.py:26-42) and reads the
+// As soon as the eager winner is known (engine.py:201-205) the prefetch warps
+// (1 or 2, PFW) leave the iteration's sort + merge to the other warps and, for
+// the winner's adjacency row,
+//   * load the neighbour ids and the degree (the candidate winners' rows were
+//     already asked of L2 at expand / survivor time),
+//   * hash every id into its two Bloom slots (bloom.py:26-42) and read the
 //     slots' pre-state bits -- every set of this row is already performed
 //     (the fetch-or results were consumed before the collision barrier),
-//   * asks L2 for the neighbours' PQ code rows (bulk prefetch),
-// and leaves ids, slots and bits in shared memory.  The next iteration then
-// starts from shared memory: its Bloom test needs no global load and its code
-// gathers hit L2.  Everything else -- table, ADC, exact in-row collision
-// replay, sort, merge, convergence, re-rank -- is search_cta_kernel's, bit for
-// bit.
+//   * stage the neighbours' PQ code rows into shared memory with cp.async
+//     (or, when they do not fit, ask L2 for them),
+// and leave ids, slots, bits and codes in shared memory.  The next iteration
+// then starts from shared memory only: no global load precedes its Bloom test
+// or its ADC.  Everything else -- table, ADC, exact in-row collision replay,
+// sort, merge, convergence, re-rank -- is search_cta_kernel's, bit for bit
+// (SURVEY.md 8(a0)).
 //
-// Filters are cleared with whole-line stores at query start (no zero-on-
-// first-touch stores), so a slot's pre-state is its word bit when the word is
-// marked in the summary and 0 otherwise, exactly as in search_cta_kernel.
+// Filters are cleared with whole-line stores at query start, so every probe
+// reads its word (no summary bitmap; its shared memory holds the staged rows).
 #pragma once
 
 #include "bang_search_cta.cuh"
@@ -72,7 +74,7 @@ __device__ __forceinline__ long long clock_after(int v) {
 // s_nfl (bit0 = pre-state bit, bit1 = word marked in the summary), ndeg; the
 // code rows are prefetched into L2.
 template <int NT, int MV, int PFW>
-__device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int lane, const uint32_t *s_sum,
+__device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int lane, uint8_t *s_code,
                                        const uint32_t *bits, uint32_t *s_nid, uint32_t *s_nps,
                                        uint8_t *s_nfl, uint32_t *s_dup, PfMisc *s_m) {
     constexpr int PL = NT / (64 * PFW);  // neighbour slots per lane (RPAD = NT/2 over PFW warps)
@@ -101,7 +103,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
         i1[r] = i2[r] = false;
         if (jj < deg) {
             const uint8_t *crow = p.codes + (int64_t)nid[r] * M;
-            if (p.pf_l2 == 1) {
+            if (p.pf_stage) {
+#pragma unroll
+                for (int v = 0; v < MV; ++v) __pipeline_memcpy_async(s_code + jj * M + v * 16, crow + v * 16, 16);
+            } else if (p.pf_l2 == 1) {
                 l2_prefetch_bulk(crow, M);
             } else if (p.pf_l2 == 2) {
                 l2_prefetch(crow);
@@ -109,10 +114,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
             }
             ps1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
             ps2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
-            i1[r] = sum_get(s_sum, ps1[r] >> 5);
-            i2[r] = sum_get(s_sum, ps2[r] >> 5);
-            if (i1[r]) wd1[r] = __ldcg(bits + (ps1[r] >> 5));
-            if (i2[r]) wd2[r] = __ldcg(bits + (ps2[r] >> 5));
+            // the filter was cleared at query start: every word is current
+            i1[r] = i2[r] = true;
+            wd1[r] = __ldcg(bits + (ps1[r] >> 5));
+            wd2[r] = __ldcg(bits + (ps2[r] >> 5));
         }
     }
     if (p.profile == 2 && lane == 0) {  // (breakdown) hashes + Bloom word arrival
@@ -151,6 +156,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
         s_nfl[2 * jj + 1] = (uint8_t)(((wd2[r] >> (ps2[r] & 31)) & 1u) | (i2[r] ? 2u : 0u) | (sh2[r] ? 4u : 0u));
     }
     if (lane == 0) s_m->ndeg = deg;
+    if (p.pf_stage) {
+        __pipeline_commit();
+        __pipeline_wait_prior(0);  // staged rows land before the iteration's barrier
+    }
 }
 
 template <int NT, int SUB, int MV, int PFW>
@@ -176,8 +185,8 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     uint32_t *s_nid = reinterpret_cast<uint32_t *>(smem + p.off_fid);
     uint8_t *s_fl = smem + p.off_alive;
     uint8_t *s_vis = smem + p.off_vis;
-    uint32_t *s_sum = reinterpret_cast<uint32_t *>(smem + p.off_sum);
     float *s_tab = reinterpret_cast<float *>(smem + p.off_tab);
+    uint8_t *s_code = smem + p.off_code;  // next row's code rows (pf_stage)
     uint32_t *s_nps = reinterpret_cast<uint32_t *>(smem + p.off_dup);
     uint8_t *s_nfl = smem + p.off_dup + 4 * NT;
     uint32_t *s_dup = reinterpret_cast<uint32_t *>(smem + p.off_dup + 5 * NT);  // warp 0's slot table
@@ -192,7 +201,8 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     const bool prof = p.profile && tc == 0;
     if (tc == 0)
         for (int i = 0; i < 8; ++i) s_m->ph[i] = 0;
-    for (int i = tid; i < kDupSlots; i += NT) s_dup[i] = kDupEmpty;  // (barrier at the query fetch)
+    if (p.pf_red)  // the slot-sharing table exists only then
+        for (int i = tid; i < kDupSlots; i += NT) s_dup[i] = kDupEmpty;  // (barrier at the query fetch)
 #define BANG_PF_PHASE(i)                                       \
     if (prof) {                                                \
         const long long now_ = clock64();                      \
@@ -209,7 +219,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         const int64_t qid = p.query_map ? (int64_t)p.query_map[qi] : qi;
 
         for (int i = tid; i < p.dim; i += NT) s_q[i] = __ldg(p.queries + qid * p.dim + i);
-        for (int i = tid; i < p.sum_words; i += NT) s_sum[i] = 0u;
         for (int i = tid; i < t; i += NT) s_vis[i] = 0;
         {   // the filter starts empty (whole-line stores)
             uint4 *b4 = reinterpret_cast<uint4 *>(bits);
@@ -249,8 +258,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 __stcg(bits + w1, b1);
                 __stcg(bits + w2, b2);
             }
-            s_sum[w1 >> 5] |= 1u << (w1 & 31);
-            s_sum[w2 >> 5] |= 1u << (w2 & 31);
         }
         __syncthreads();
         if (tid == 0) {  // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125)
@@ -259,7 +266,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
             s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
         }
-        if (pfw) pf_row<NT, MV, PFW>(p, (uint32_t)p.medoid, tid, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+        if (pfw) pf_row<NT, MV, PFW>(p, (uint32_t)p.medoid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
@@ -298,7 +305,18 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             // (L2) in flight while the Bloom test runs
             uint32_t id = 0, ps = 0, cw[MHW];
             uint32_t fl = 0;
-            if (valid) {
+            if (valid && p.pf_stage) {
+                id = s_nid[j];
+                ps = s_nps[tid];
+                fl = s_nfl[tid];
+                const uint32_t *row = reinterpret_cast<const uint32_t *>(s_code + j * M) + h * MHW;
+#pragma unroll
+                for (int q = 0; q < MHW; q += 2) {
+                    const uint2 v = *reinterpret_cast<const uint2 *>(row + q);
+                    cw[q] = v.x;
+                    cw[q + 1] = v.y;
+                }
+            } else if (valid) {
                 id = s_nid[j];
                 ps = s_nps[tid];
                 fl = s_nfl[tid];
@@ -317,11 +335,9 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             }
             // ---- kernel 2: Bloom test of this half's slot (pre-state)
             const uint32_t mybit = fl & 1u;
-            const bool init = (fl & 2u) != 0;
             const uint32_t pbit = __shfl_xor_sync(kFull, mybit, 1);
             const uint32_t pps = __shfl_xor_sync(kFull, ps, 1);
             bool fresh = valid && !(mybit && pbit);
-            if (fresh && !init) sum_set(s_sum, ps >> 5);
             BANG_PF_PHASE(0)  // (phase 1, the zeroing barrier, does not exist here)
             // pf_red: fire-and-forget sets, in-row slot sharing known from
             // warp 0's table; else the fetch-or result tells
@@ -414,7 +430,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 // ---- one hop ahead: the winner's row while warps PFW.. sort + merge
                 named_bar_arrive(1, NT);
                 const long long c0 = p.profile ? clock64() : 0;
-                if (winner != kSentinel) pf_row<NT, MV, PFW>(p, wid, tid, s_sum, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+                if (winner != kSentinel) pf_row<NT, MV, PFW>(p, wid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
                 if (p.profile && tid == 0) s_m->ph[1] += (unsigned long long)(clock_after(s_nfl[0]) - c0);
             } else {
                 named_bar_sync(1, NT);  // all survivors published
