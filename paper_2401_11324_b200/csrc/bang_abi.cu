@@ -199,11 +199,17 @@ const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr = false) {
     return nullptr;
 }
 
-const void *pick_pf_kernel(int nt, int sub, int mv, int pfw = 1) {
-#define BANG_P(N, S, V)                                                                            \
-    if (nt == N && sub == S && mv == V)                                                            \
-        return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2>)            \
-                        : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1>);
+template <int N, int S, int V>
+const void *pf_kernel_ptr(int pfw, bool stage) {
+    if (stage) return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2, true>)
+                               : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1, true>);
+    return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2, false>)
+                    : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1, false>);
+}
+
+const void *pick_pf_kernel(int nt, int sub, int mv, int pfw = 1, bool stage = false) {
+#define BANG_P(N, S, V) \
+    if (nt == N && sub == S && mv == V) return pf_kernel_ptr<N, S, V>(pfw, stage);
     BANG_P(128, 4, 2) BANG_P(256, 4, 2)
     BANG_P(128, 2, 3) BANG_P(256, 2, 3)
     BANG_P(128, 0, 2) BANG_P(256, 0, 2)
@@ -437,7 +443,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
         const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                          : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw)
+                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
                                           : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
         if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
@@ -567,7 +573,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     }
     const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
                       : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw)
+                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
                       : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv, p.row_hdr != 0)
                       : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
                                       : pick_kernel(pl.npl, pl.sub, pl.mv);

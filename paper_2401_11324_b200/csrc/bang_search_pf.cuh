@@ -162,7 +162,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     }
 }
 
-template <int NT, int SUB, int MV, int PFW>
+// STAGE: the next row's code rows are staged in smem (p.pf_stage); a template
+// parameter so the staged instance has no global code-load path whose
+// scoreboard the compiler could merge with the fetch-or's
+template <int NT, int SUB, int MV, int PFW, bool STAGE>
 __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kernel(const SearchParams p) {
     constexpr int NW = NT / 32;
     constexpr int NC = NT - 32 * PFW;  // sort/merge threads (warps PFW..)
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             // (L2) in flight while the Bloom test runs
             uint32_t id = 0, ps = 0, cw[MHW];
             uint32_t fl = 0;
-            if (valid && p.pf_stage) {
+            if (STAGE && valid) {
                 id = s_nid[j];
                 ps = s_nps[tid];
                 fl = s_nfl[tid];
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                     cw[q] = v.x;
                     cw[q + 1] = v.y;
                 }
-            } else if (valid) {
+            } else if (!STAGE && valid) {
                 id = s_nid[j];
                 ps = s_nps[tid];
                 fl = s_nfl[tid];
