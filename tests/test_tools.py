@@ -125,3 +125,25 @@ def test_artifact_cache_roundtrip(tmp_path):
     assert isinstance(art["graph"], GraphIndex) and art["graph"].medoid == 3
     assert isinstance(art["codebook"], PQCodebook) and art["codebook"].centroids[1].shape == (256, 2)
     assert isinstance(art["codes"], CompressedVectors)
+
+
+def test_locality_order_relabel_is_an_isomorphism():
+    """graph_build.locality_order + relabel_index rename nodes only: every
+    edge, degree, vector and the medoid survive under the permutation, and
+    nodes of one k-means cell end up contiguous."""
+    import torch
+    base, _ = gaussian_mixture(3_000, 0, 16, clusters=30, seed=4)
+    g = gb.build_graph(base, degree_bound=12, seed=4, device=torch.device("cpu"))
+    perm = gb.locality_order(base, nlist=8, seed=4, device=torch.device("cpu"))
+    assert np.array_equal(np.sort(perm), np.arange(base.shape[0]))
+    b2, adj2, deg2, med2 = gb.relabel_index(perm, base, g.adjacency, g.degrees, g.medoid,
+                                            device=torch.device("cpu"))
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(perm.size)
+    assert np.array_equal(b2, base[perm]) and np.array_equal(deg2, g.degrees[perm])
+    assert med2 == inv[g.medoid]
+    for new in range(0, perm.size, 97):
+        old = perm[new]
+        d = g.degrees[old]
+        assert np.array_equal(adj2[new, :d], inv[g.adjacency[old, :d]])
+        assert np.all(adj2[new, d:] == -1)
