@@ -60,3 +60,17 @@ def to_host(t, dtype=None) -> np.ndarray:
 def stream():
     import torch
     return torch.cuda.current_stream(torch_device())
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """Host array in page-locked memory (torch's caching host allocator, so
+    repeated searches reuse the pages; the array keeps its block alive).
+    Device->host copies into it run at PCIe speed instead of being staged
+    through the driver's bounce buffers."""
+    if os.environ.get("BANG_PAGEABLE_OUT") == "1":  # (measurement: the pageable baseline)
+        return np.empty(shape, dtype)
+    import torch
+    tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.int32): torch.int32,
+           np.dtype(np.int64): torch.int64, np.dtype(np.uint8): torch.uint8,
+           np.dtype(np.float64): torch.float64}[np.dtype(dtype)]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()

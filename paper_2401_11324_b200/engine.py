@@ -182,8 +182,9 @@ class DeviceIndex:
     def search(self, queries: np.ndarray, k: int, t: int, bloom_entries: int, flags: int):
         q = np.ascontiguousarray(queries, dtype=np.float32)
         nq = q.shape[0]
-        ids = np.empty((nq, k), np.int32)
-        dists = np.empty((nq, k), np.float32)
+        # the large device->host results land in page-locked memory
+        ids = _dev.pinned_empty((nq, k), np.int32)
+        dists = _dev.pinned_empty((nq, k), np.float32)
         iters = np.empty(nq, np.int32)
         conv = np.empty(nq, np.uint8)
         short = np.empty(nq, np.uint8)
@@ -194,7 +195,7 @@ class DeviceIndex:
                            _lib.ptr(dists), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(short),
                            _lib.ptr(wall), _lib.ptr(offs), None, 0)
         _lib.check(st, "bang_search")
-        flat = np.empty(int(offs[-1]), np.int32)
+        flat = _dev.pinned_empty(int(offs[-1]), np.int32)
         _lib.check(L.bang_last_visit_logs(self.handle, _lib.ptr(flat), flat.size), "bang_last_visit_logs")
         return ids, dists, iters, conv.astype(bool), short.astype(bool), wall, offs, flat
 
