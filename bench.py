@@ -260,6 +260,21 @@ def main():
                 break
         if not t_sel:
             t_sel = T_SWEEP[-1]
+        elif len(sweep) > 1:
+            # the operating point at unit granularity: bisect (t_prev, t_sel]
+            # for the smallest t whose recall still meets the target
+            lo, hi = sweep[-2]["t"], t_sel
+            while hi - lo > 1:
+                mid = (lo + hi) // 2
+                searcher.t = mid
+                res = searcher.search(shard["queries"])
+                r = recall(res.ids, shard["gt_ids"], k)
+                sweep.append({"t": mid, "recall": round(r, 4), "mean_iters": float(res.iterations.mean())})
+                if r >= args.target_recall:
+                    hi = mid
+                else:
+                    lo = mid
+            t_sel = hi
     if world > 1:
         tt = torch.tensor([t_sel], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
