@@ -411,17 +411,24 @@ def main():
     s_last = stats[-1]
     avg_kern_ms = float(np.mean(kern_ms))
     achieved = s_last["algorithmic_bytes"] / (avg_kern_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, traffic_note = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             kname = _lib.KERNELS.get(s_last.get("kernel", 0), "?")
             tr = json.load(f).get(f"{args.config}/{kname}")
             if tr and tr.get("t") == t_sel:
                 traffic = tr["dram_bytes_per_launch"]
+                traffic_note = f"ncu capture at t={t_sel}: {tr.get('source', '')}"
+            elif tr and tr.get("iterations"):
+                # the capture's DRAM bytes per query-iteration x this launch's iterations
+                traffic = int(round(tr["dram_bytes_per_launch"] / tr["iterations"] * s_last["iterations"]))
+                traffic_note = (f"scaled from the ncu capture at t={tr['t']} ({tr['dram_bytes_per_launch']} B over "
+                                f"{tr['iterations']} iterations) to this launch's {s_last['iterations']} iterations")
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_note,
+                "peak_kind": peak_kind,
                 "kernel": "bang::" + _lib.KERNELS.get(s_last.get("kernel", 0), "?"), "kernel_ms": round(avg_kern_ms, 4),
                 "algorithmic_bytes": s_last["algorithmic_bytes"],
                 "adc_bytes": s_last["adc_bytes"],
