@@ -274,7 +274,28 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         uint32_t u = (uint32_t)p.medoid;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         int iters = 0;
+        // ---- expand u (engine.py:163-178) by the first sort/merge warp: mark
+        // it visited, log it, find the next unvisited entry (the eager head)
+        // and start the head's row towards L2.  In the loop this runs at the
+        // end of the merge, before the iteration's last barrier.
+        auto expand = [&](int up, uint32_t uu, int cnt_, int it_) {
+            if (lane == 0) {
+                if (p.debug && key_id(s_wl[up]) != uu) atomicAdd(p.counters + kCtrDebugFail, 1ull);
+                s_vis[up] = 1;
+                if (it_ < p.log_cap) log[it_] = (int32_t)uu;
+            }
+            __syncwarp();
+            const int hp = first_unvisited(s_vis, up + 1, cnt_);
+            if (lane == 0) {
+                s_m->hpos = hp;
+                s_m->head = hp < cnt_ ? s_wl[hp] : kSentinel;
+                // the head is the next winner unless a fresh neighbour beats
+                // it: start its row towards L2 now
+                if (p.pf_spec && hp < cnt_) prefetch_row_l2(p, key_id(s_wl[hp]));
+            }
+        };
         __syncthreads();
+        if (warp == PFW) expand(0, u, 1, 0);
         if (prof) {  // query prologue (filter clear, table, medoid row) -> slot 7
             const long long now_ = clock_after(s_m->ndeg);
             s_m->ph[7] += (unsigned long long)(now_ - s_m->t_ph);
@@ -282,25 +303,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         }
 
         for (;;) {
-            // ---- expand u (engine.py:163-178); warp 0 finds the next
-            // unvisited entry after u (the eager "head")
-            if (warp == 0) {
-                if (lane == 0) {
-                    if (p.debug && key_id(s_wl[upos]) != u) atomicAdd(p.counters + kCtrDebugFail, 1ull);
-                    s_vis[upos] = 1;
-                    if (iters < p.log_cap) log[iters] = (int32_t)u;
-                }
-                __syncwarp();
-                const int hp = first_unvisited(s_vis, upos + 1, cnt);
-                if (lane == 0) {
-                    s_m->hpos = hp;
-                    s_m->head = hp < cnt ? s_wl[hp] : kSentinel;
-                    // the head is the next winner unless a fresh neighbour beats
-                    // it: start its row towards L2 now
-                    if (p.pf_spec && hp < cnt) prefetch_row_l2(p, key_id(s_wl[hp]));
-                }
-            }
-            ++iters;
+            ++iters;  // u was expanded (logged, marked) before the last barrier
             const int deg = s_m->ndeg;
             st_probes += deg;
             const bool valid = j < deg;
@@ -491,6 +494,11 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                         s_wl[spos] = sk;
                         s_vis[spos] = 0;
                     }
+                }
+                named_bar_sync(2, NC);  // the merged worklist is complete
+                if (warp == PFW) {
+                    const int wp = s_m->wpos;
+                    if (wp < t) expand(wp, wid, min(t, cnt + n), iters);
                 }
             }
             cnt = min(t, cnt + n);
