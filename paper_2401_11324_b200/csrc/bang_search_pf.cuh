@@ -81,6 +81,8 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
     constexpr int PT = 32 * PFW;         // prefetch threads; lane = index among them
     constexpr int M = 16 * MV;
     const long long c0 = p.profile == 2 ? clock64() : 0;
+    if (p.profile == 2)  // (breakdown) the row loads issue after c0
+        asm volatile("mov.b32 %0, %0;" : "+r"(w) : "l"(c0));
     const int deg = p.deg[w];
     uint32_t nid[PL];
 #pragma unroll
