@@ -97,6 +97,9 @@ struct SearchParams {
     // search_pf_kernel: the prefetch warps stage the next row's code rows at
     // off_code (rpad x 16*MV bytes) instead of prefetching them into L2
     int32_t pf_stage, off_code;
+    // search_pf_kernel: two-hop speculative L2 prefetch of the head's
+    // neighbours' code rows (BANG_PF_SPEC2)
+    int32_t pf_spec2;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

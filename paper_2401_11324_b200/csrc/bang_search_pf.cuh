@@ -306,6 +306,16 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
 
         for (;;) {
             ++iters;  // u was expanded (logged, marked) before the last barrier
+            // two hops ahead (speculative): if the head wins this iteration,
+            // its neighbours' code rows are the next prefetch's HBM gathers.
+            // Read the head's row now (it was sent towards L2 at expand) and,
+            // after the ADC, ask L2 for those code rows.
+            int32_t spec_nb = -1;
+            // (iteration 1: the prologue's expand is still writing the head)
+            if (p.pf_spec2 && iters > 1 && h == 0 && j < p.R) {
+                const uint64_t hd = s_m->head;
+                if (hd != kSentinel) spec_nb = __ldcg(p.adj + (int64_t)key_id(hd) * p.adj_stride + j);
+            }
             const int deg = s_m->ndeg;
             st_probes += deg;
             const bool valid = j < deg;
@@ -396,6 +406,11 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                     s_m->wfresh[warp] = __popc(fb);
                     // this warp's best fresh neighbour may be the next winner
                     if (p.pf_spec && pass == 0 && wm != kSentinel) prefetch_row_l2(p, key_id(wm));
+                }
+                if (pass == 0 && spec_nb >= 0) {  // (adjacency rows are -1 padded)
+                    const uint8_t *crow = p.codes + (int64_t)spec_nb * M;
+                    l2_prefetch(crow);
+                    if (((uintptr_t)crow & 31u) + M > 32u) l2_prefetch(crow + M - 1);
                 }
                 BANG_PF_PHASE(2)
                 const int any_coll = __syncthreads_or(coll);
