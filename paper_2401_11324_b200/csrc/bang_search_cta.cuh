@@ -103,7 +103,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
     uint64_t *s_wl = reinterpret_cast<uint64_t *>(smem + p.off_wl);
     uint64_t *s_sk = reinterpret_cast<uint64_t *>(smem + p.off_sk);
     uint64_t *s_nk = reinterpret_cast<uint64_t *>(smem + p.off_nk);
-    uint32_t *s_ids = reinterpret_cast<uint32_t *>(smem + p.off_fid);
     uint8_t *s_fl = smem + p.off_alive;
     uint8_t *s_vis = smem + p.off_vis;
     uint32_t *s_sum = reinterpret_cast<uint32_t *>(smem + p.off_sum);
