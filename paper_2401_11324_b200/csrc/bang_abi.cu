@@ -558,6 +558,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
         p.pf_spec = !(ps && *ps == '0');
         const char *ps2 = getenv("BANG_PF_SPEC2");
         p.pf_spec2 = ps2 && *ps2 == '1';  // measured neutral at C3 (795K vs 797K)
+        const char *pea = getenv("BANG_PF_EARLY");
+        p.pf_early = !pl.pf_red && !(pea && *pea == '0');
         const char *pe = getenv("BANG_PF_EAGER");
         p.pf_eager = pe && *pe == '1';
     }

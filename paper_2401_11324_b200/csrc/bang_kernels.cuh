@@ -100,6 +100,9 @@ struct SearchParams {
     // search_pf_kernel: two-hop speculative L2 prefetch of the head's
     // neighbours' code rows (BANG_PF_SPEC2)
     int32_t pf_spec2;
+    // search_pf_kernel: the prefetch warps perform the next row's Bloom sets
+    // (fetch-or) one iteration ahead (BANG_PF_EARLY)
+    int32_t pf_early;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

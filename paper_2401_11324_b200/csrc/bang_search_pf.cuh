@@ -141,12 +141,46 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
             if (ps2[r] != ps1[r]) sh2[r] = dup_claim(s_dup, ps2[r], &d2[r]);
         }
     }
-    if (PFW == 1) __syncwarp();
-    else named_bar_sync(3, PT);
+    if (p.pf_red) {
+        if (PFW == 1) __syncwarp();
+        else named_bar_sync(3, PT);
 #pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        if (d1[r] >= 0) s_dup[d1[r]] = kDupEmpty;
-        if (d2[r] >= 0) s_dup[d2[r]] = kDupEmpty;
+        for (int r = 0; r < PL; ++r) {
+            if (d1[r] >= 0) s_dup[d1[r]] = kDupEmpty;
+            if (d2[r] >= 0) s_dup[d2[r]] = kDupEmpty;
+        }
+    }
+    // early Bloom sets (p.pf_early): the row's presumed-fresh probes set their
+    // bits now, one iteration ahead of their test (the test reads the
+    // pre-state bits above, and no other row of this query runs in between).
+    // A fetch-or that finds its bit set though the pre-state did not have it
+    // marks in-row slot sharing for the exact replay -- the same evidence the
+    // compute threads' fetch-or gave, without its round trip on their path.
+    if (p.pf_early) {
+        uint32_t o1[PL], o2[PL];
+        bool fr[PL];
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            const uint32_t b1 = (wd1[r] >> (ps1[r] & 31)) & 1u, b2 = (wd2[r] >> (ps2[r] & 31)) & 1u;
+            fr[r] = lane + PT * r < deg && !(b1 && b2);  // (consumes this thread's word loads)
+        }
+        // every prefetch warp holds its pre-state words before any set of the
+        // row lands (one warp: program order already guarantees it)
+        if (PFW > 1) named_bar_sync(3, PT);
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            o1[r] = o2[r] = 0u;
+            if (fr[r]) {
+                o1[r] = atomicOr(const_cast<uint32_t *>(bits) + (ps1[r] >> 5), 1u << (ps1[r] & 31));
+                if (ps2[r] != ps1[r]) o2[r] = atomicOr(const_cast<uint32_t *>(bits) + (ps2[r] >> 5), 1u << (ps2[r] & 31));
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            const uint32_t b1 = (wd1[r] >> (ps1[r] & 31)) & 1u, b2 = (wd2[r] >> (ps2[r] & 31)) & 1u;
+            sh1[r] = fr[r] && !b1 && ((o1[r] >> (ps1[r] & 31)) & 1u);
+            sh2[r] = fr[r] && ps2[r] != ps1[r] && !b2 && ((o2[r] >> (ps2[r] & 31)) & 1u);
+        }
     }
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
@@ -361,7 +395,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             // warp 0's table; else the fetch-or result tells
             uint32_t old = 0;
             const bool do_atom = fresh && !(h == 1 && pps == ps);
-            if (do_atom) {
+            if (do_atom && !p.pf_early) {  // (pf_early: set one iteration ahead by the prefetch warps)
                 if (p.pf_red) atomicOr(bits + (ps >> 5), 1u << (ps & 31));
                 else old = atomicOr(bits + (ps >> 5), 1u << (ps & 31));
             }
@@ -399,7 +433,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 // Bloom collision check (fetch-or results) folded into the barrier
                 // (the fetch-or result is consumed only here, after the ADC)
                 const bool coll = pass == 0 && do_atom && !mybit &&
-                                  (p.pf_red ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0);
+                                  ((p.pf_red || p.pf_early) ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0);
                 if (lane == 0) {
                     s_m->wmin[warp] = wm;
                     s_m->wcnt[warp] = __popc(sb);

@@ -366,7 +366,7 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("pf", ["1", "0", "red", "pf2", "red2", "l2", "spec2"])
+@pytest.mark.parametrize("pf", ["1", "0", "red", "pf2", "red2", "l2", "spec2", "late"])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, pf, monkeypatch):
     """Default CTA kernel with small Bloom filters: most rows share slots, so
     the warp replay from pre-state bits (replay_row_warp) runs constantly.
@@ -378,6 +378,7 @@ def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, p
     monkeypatch.setenv("BANG_PF_WARPS", "2" if pf.endswith("2") else "1")  # 2: two prefetch warps
     monkeypatch.setenv("BANG_PF_STAGE", "0" if pf == "l2" else "1")  # l2: code rows via L2, not smem
     monkeypatch.setenv("BANG_PF_SPEC2", "1" if pf == "spec2" else "0")  # two-hop speculative code prefetch
+    monkeypatch.setenv("BANG_PF_EARLY", "0" if pf == "late" else "1")  # late: Bloom sets by the compute threads
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
