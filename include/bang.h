@@ -52,14 +52,31 @@ typedef int32_t bang_status;
 #define BANG_TABLE_SMEM 16     /* ADC from a per-query table in shared memory         */
 #define BANG_CODEBOOK_SMEM 32  /* ADC recomputing entries from a CTA-shared codebook  */
 #define BANG_PROFILE_PHASES 64 /* accumulate per-phase cycles (diagnostics, slower)  */
-#define BANG_DEBUG_GENERIC 128 /* use the generic search kernel even where a specialised one exists */
-#define BANG_WARP_PER_QUERY 256 /* smem-table ADC with one warp per query instead of one CTA */
-#define BANG_QUERY_POOL 512    /* lockstep query pool per CTA, CTA-shared codebook ADC        */
-#define BANG_NO_POOL 1024      /* never pick the query-pool kernel automatically               */
-#define BANG_NO_FAT 2048       /* do not use the fat-row (inline neighbour codes) CTA kernel  */
-#define BANG_PIPELINE_ROWS 4096 /* CTA kernel with the next row's loads issued during the merge */
 /* (no ADC flag: the per-query smem table when >= 4 queries fit per SM, else
  *  the shared codebook, else the HBM table)                                */
+
+/* Search kernels (bang_options.kernel; bang_search_stats.kernel reports the
+ * one that ran as 0 search_kernel, 2 search_cta_kernel, 6 search_pf_kernel). */
+#define BANG_KERNEL_AUTO 0 /* pf when the codes exceed L2 and R > 32, else cta; warp otherwise */
+#define BANG_KERNEL_WARP 1 /* search_kernel: one warp per query, every ADC data flow           */
+#define BANG_KERNEL_CTA 2  /* search_cta_kernel: one CTA per query, per-query smem table       */
+#define BANG_KERNEL_PF 3   /* search_pf_kernel: search_cta_kernel + prefetch warps one hop ahead */
+
+/* Per-index tuning (bang_index_set_options); every setting gives identical
+ * results -- they only move work between warps and memory levels.
+ * bang_options_default() fills the measured-best defaults.               */
+typedef struct bang_options {
+    int32_t kernel;      /* BANG_KERNEL_*                                               */
+    int32_t pf_warps;    /* search_pf_kernel prefetch warps: 0 auto, 1 or 2             */
+    int32_t pf_stage;    /* 1: next row's code rows staged in smem when they fit; 0: L2 */
+    int32_t pf_early;    /* 1: the prefetch warps perform the next row's Bloom sets     */
+    int32_t pf_spec;     /* 1: L2 prefetch of the candidate winners' adjacency rows     */
+    int32_t bloom_clear; /* 1: search_cta_kernel clears its filter per query; 0: smem
+                            summary bitmap of the words this query wrote               */
+    int32_t l2_persist;  /* 1: the Bloom filters get an L2-persisting access window      */
+    int32_t profile;     /* with BANG_PROFILE_PHASES: 2 = the prefetch warps' stages     */
+    int32_t reserved[8];
+} bang_options;
 
 typedef struct bang_index bang_index;
 
@@ -82,8 +99,7 @@ typedef struct bang_search_stats {
                                  summed over warps: 0 adjacency wait, 1 expand,
                                  2 Bloom issue, 3 ADC, 4 Bloom resolve, 5 sort +
                                  eager + prefetch, 6 merge + converge, 7 unused */
-    int32_t kernel;           /* 0 warp/query, 1 warp/query smem table, 2 CTA/query,
-                                 3 CTA/query over fat rows, 4 query pool         */
+    int32_t kernel;           /* 0 search_kernel, 2 search_cta_kernel, 6 search_pf_kernel */
     int32_t reserved;
 } bang_search_stats;
 
@@ -119,10 +135,19 @@ bang_status bang_index_info(const bang_index *index, int32_t *device, int64_t *n
                             int32_t *dim, int32_t *R);
 /* Device pointers owned by the handle (for the per-kernel entries).  With
  * BANG_GRAPH_HOST_MAPPED and R % 4 == 0 the adjacency rows have a stride of
- * R + 4 int32: a 16-byte [deg, 0, 0, 0] header precedes each row. */
+ * R + 4 int32: a 16-byte [deg, 0, 0, 0] header precedes each row.  Code row
+ * i starts at codes + i * bang_index_code_stride(index). */
 bang_status bang_index_device_ptrs(const bang_index *index, const uint8_t **codes,
                                    const float **centroids, const int32_t **adjacency,
                                    const int32_t **degrees, const void **vectors);
+/* Bytes between device code rows: m, except m = 48 rows padded to 64 bytes
+ * (one aligned DRAM burst per gathered row). */
+int32_t bang_index_code_stride(const bang_index *index);
+/* Tuning of the searches on this handle (kernel choice and the prefetch
+ * kernel's data flows); see bang_options.  Results never depend on it. */
+void bang_options_default(bang_options *options);
+bang_status bang_index_set_options(bang_index *index, const bang_options *options);
+bang_status bang_index_get_options(const bang_index *index, bang_options *options);
 
 /* ------------------------------------------------------ batched search
  * GraphSearcher.search for one batch (engine.py:409-452): queries host
@@ -163,6 +188,11 @@ bang_status bang_search_device(bang_index *index, const float *d_queries, int64_
 bang_status bang_sync_status(bang_index *index);
 
 /* ---------------------------------------------- per-kernel entries (device pointers) */
+
+/* Kernel 1 with host buffers -- build_pq_dist_table(queries, codebook)
+ * (pq.py:299-319) on the handle's codebook: queries (nq, dim) f32 host,
+ * out (nq, m, 256) f32 host, caller-allocated. */
+bang_status bang_pq_table(bang_index *index, const float *queries, int64_t nq, float *out);
 
 /* Kernel 1 -- build_pq_dist_table (pq.py:284-319): out (nq, m, 256) f32,
  * entry = ((d0*d0 + d1*d1) + ...) in f32 without FMA.  sub_sizes is HOST. */

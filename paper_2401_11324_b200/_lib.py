@@ -32,19 +32,27 @@ TABLE_GLOBAL = 8
 TABLE_SMEM = 16
 CODEBOOK_SMEM = 32
 PROFILE_PHASES = 64
-DEBUG_GENERIC = 128
-WARP_PER_QUERY = 256
-QUERY_POOL = 512
-NO_POOL = 1024
-NO_FAT = 2048
-PIPELINE_ROWS = 4096
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
-KERNELS = {0: "search_kernel", 1: "search_tab_kernel", 2: "search_cta_kernel", 3: "search_fat_kernel",
-           4: "search_pool_kernel", 5: "search_ctapipe_kernel", 6: "search_pf_kernel"}
+# bang_search_stats.kernel -> kernel name
+KERNELS = {0: "search_kernel", 2: "search_cta_kernel", 6: "search_pf_kernel"}
+# bang_options.kernel
+KERNEL_CHOICES = {"auto": 0, "warp": 1, "cta": 2, "pf": 3}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
+
+
+class Options(ctypes.Structure):
+    """bang_options (include/bang.h): per-index kernel choice and tuning."""
+    _fields_ = [
+        ("kernel", ctypes.c_int32), ("pf_warps", ctypes.c_int32), ("pf_stage", ctypes.c_int32),
+        ("pf_early", ctypes.c_int32), ("pf_spec", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
+        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8),
+    ]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
 
 
 class SearchStats(ctypes.Structure):
@@ -75,6 +83,11 @@ _SIGS = {
     "bang_index_destroy": (None, [_P]),
     "bang_index_info": (_I32, [_P, _P, _P, _P, _P, _P]),
     "bang_index_device_ptrs": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "bang_index_code_stride": (_I32, [_P]),
+    "bang_options_default": (None, [ctypes.POINTER(Options)]),
+    "bang_index_set_options": (_I32, [_P, ctypes.POINTER(Options)]),
+    "bang_index_get_options": (_I32, [_P, ctypes.POINTER(Options)]),
+    "bang_pq_table": (_I32, [_P, _P, _I64, _P]),
     "bang_search": (_I32, [_P, _P, _I64, _I32, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P, _P,
                            _P, _I64]),
     "bang_last_visit_logs": (_I32, [_P, _P, _I64]),

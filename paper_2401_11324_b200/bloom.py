@@ -58,12 +58,10 @@ class BloomFilterBank:
         return _dev.to_host(self._bits, np.uint64)
 
     def set_all_rows(self, node_id: int) -> None:
-        """bloom.py:87-92: mark one id in every filter (the entry point)."""
-        p1, p2 = bit_positions(np.asarray([node_id]), self.entries)
-        for p in (int(p1[0]), int(p2[0])):
-            col = self._bits[:, p >> 6]
-            bit = np.int64(np.uint64(1) << np.uint64(p & 63))  # two's complement for bit 63
-            col |= int(bit)
+        """bloom.py:87-92: mark one id in every filter (the entry point).
+        Through kernel 2: testing-and-setting the id in every row sets both
+        of its bits in every row (already-set bits stay set)."""
+        self.filter_and_set(np.arange(self.count, dtype=np.int64), np.full(self.count, int(node_id), np.int64))
 
     def filter_and_set(self, rows, node_ids) -> np.ndarray:
         """bloom.py:124-163: test-and-set every (row, id) probe, equal rows in

@@ -12,17 +12,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/bang.h"
 #include "bang_kernels.cuh"
-#include "bang_search_tab.cuh"
-#include "bang_search_cta.cuh"
-#include "bang_search_pool.cuh"
-#include "bang_search_fat.cuh"
-#include "bang_search_ctapipe.cuh"
-#include "bang_search_pf.cuh"
+#include "bang_pick.h"
+#include "bang_standalone.cuh"
 
 using namespace bang;
 
@@ -99,12 +97,12 @@ struct bang_index {
     bool row_hdr = false;
     void *vectors = nullptr;
     bool host_graph = false;
-    // fat rows (bang_search_fat.cuh): ids + inline neighbour codes, HBM only
-    uint8_t *fat = nullptr;
-    int64_t fat_stride = 0;
-    int32_t fat_code_off = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bang_options opts{};
+    int32_t code_stride = 0;  // bytes between code rows (m, or 64 for m = 48)
+    int32_t k_last = 0;       // k of the last search (stats)
+    bool persist_user = false;
     int sm_count = 148;
     int max_smem = 227 * 1024;
     int64_t persist_max = 0, window_max = 0;  // L2 persistence limits of the device
@@ -137,192 +135,118 @@ struct bang_index {
 
 namespace {
 
+// stats.kernel ids (bang.h)
+enum KernelId { kKGeneric = 0, kKCta = 2, kKPf = 6 };
+
 struct Plan {
     int variant = kAdcSmemCodebook;
+    int kernel = kKGeneric;
     int npl = 2, sub = 0, mv = 0;
-    bool tab_kernel = false;  // search_tab_kernel (smem table + 16-byte code rows)
-    bool cta_kernel = false;  // search_cta_kernel (one CTA per query, smem table)
-    bool pool_kernel = false; // search_pool_kernel (query pool per CTA, smem codebook)
-    bool fat_kernel = false;  // search_fat_kernel (CTA per query over fat rows)
-    bool pipe_kernel = false; // search_ctapipe_kernel (next row's loads during the merge)
-    bool pf_kernel = false;   // search_pf_kernel (warp 0 prefetches the next row's Bloom bits)
     int pfw = 1;              // search_pf_kernel: prefetch warps
-    bool pf_red = false;      // search_pf_kernel: fire-and-forget sets
     bool pf_stage = false;    // search_pf_kernel: next row's code rows staged in smem
     int off_code = 0;
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
-    int pool_slots = 0, rr_ctas = 0;
-    int nt = 0;               // threads per CTA of the CTA kernel
+    int nt = 0;               // threads per CTA of the CTA kernels
     int warps = 32, ctas = 148, slots = 0;
     int shared_bytes = 0, per_warp = 0, smem = 0;
     int off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;
     int sum_words = 0;
     int64_t bloom_stride = 0;
+    const void *fn = nullptr;  // the kernel to launch
 };
 
-template <int NPL, int SUB, int MV>
-const void *kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_kernel<NPL, SUB, MV>);
-}
-
-template <int NPL, int SUB, int MV>
-const void *tab_kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_tab_kernel<NPL, SUB, MV>);
-}
-
-const void *pick_tab_kernel(int npl, int sub, int mv) {
-#define BANG_T(N, S, V) \
-    if (npl == N && sub == S && mv == V) return tab_kernel_ptr<N, S, V>();
-    BANG_T(1, 4, 2) BANG_T(2, 4, 2) BANG_T(4, 4, 2)
-    BANG_T(1, 2, 3) BANG_T(2, 2, 3) BANG_T(4, 2, 3)
-    BANG_T(1, 0, 2) BANG_T(2, 0, 2) BANG_T(4, 0, 2)
-    BANG_T(1, 0, 3) BANG_T(2, 0, 3) BANG_T(4, 0, 3)
-#undef BANG_T
-    return nullptr;
-}
-
-template <int NT, int SUB, int MV>
-const void *cta_kernel_ptr(bool hdr) {
-    return hdr ? reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV, true>)
-               : reinterpret_cast<const void *>(&search_cta_kernel<NT, SUB, MV, false>);
-}
-
-const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr = false) {
-#define BANG_C(N, S, V) \
-    if (nt == N && sub == S && mv == V) return cta_kernel_ptr<N, S, V>(hdr);
-    BANG_C(64, 4, 2) BANG_C(128, 4, 2) BANG_C(256, 4, 2)
-    BANG_C(64, 2, 3) BANG_C(128, 2, 3) BANG_C(256, 2, 3)
-    BANG_C(64, 0, 2) BANG_C(128, 0, 2) BANG_C(256, 0, 2)
-    BANG_C(64, 0, 3) BANG_C(128, 0, 3) BANG_C(256, 0, 3)
-#undef BANG_C
-    return nullptr;
-}
-
-template <int N, int S, int V>
-const void *pf_kernel_ptr(int pfw, bool stage) {
-    if (stage) return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2, true>)
-                               : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1, true>);
-    return pfw == 2 ? reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 2, false>)
-                    : reinterpret_cast<const void *>(&search_pf_kernel<N, S, V, 1, false>);
-}
-
-const void *pick_pf_kernel(int nt, int sub, int mv, int pfw = 1, bool stage = false) {
-#define BANG_P(N, S, V) \
-    if (nt == N && sub == S && mv == V) return pf_kernel_ptr<N, S, V>(pfw, stage);
-    BANG_P(128, 4, 2) BANG_P(256, 4, 2)
-    BANG_P(128, 2, 3) BANG_P(256, 2, 3)
-    BANG_P(128, 0, 2) BANG_P(256, 0, 2)
-    BANG_P(128, 0, 3) BANG_P(256, 0, 3)
-#undef BANG_P
-    return nullptr;
-}
-
-template <int NT, int SUB, int MV>
-const void *fat_kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_fat_kernel<NT, SUB, MV, MV == 3 ? 4 : 6>);
-}
-
-const void *pick_fat_kernel(int nt, int sub, int mv) {
-#define BANG_F(N, S, V) \
-    if (nt == N && sub == S && mv == V) return fat_kernel_ptr<N, S, V>();
-    BANG_F(64, 4, 2) BANG_F(128, 4, 2) BANG_F(64, 2, 3) BANG_F(128, 2, 3)
-#undef BANG_F
-    return nullptr;
-}
-
-template <int NT, int SUB, int MV>
-const void *pipe_kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_ctapipe_kernel<NT, SUB, MV>);
-}
-
-const void *pick_pipe_kernel(int nt, int sub, int mv) {
-#define BANG_Q(N, S, V) \
-    if (nt == N && sub == S && mv == V) return pipe_kernel_ptr<N, S, V>();
-    BANG_Q(64, 4, 2) BANG_Q(128, 4, 2) BANG_Q(256, 4, 2) BANG_Q(64, 2, 3) BANG_Q(128, 2, 3) BANG_Q(256, 2, 3)
-    BANG_Q(64, 0, 2) BANG_Q(128, 0, 2) BANG_Q(256, 0, 2) BANG_Q(64, 0, 3) BANG_Q(128, 0, 3) BANG_Q(256, 0, 3)
-#undef BANG_Q
-    return nullptr;
-}
-
-template <int SUB, int MV, int RPAD>
-const void *pool_kernel_ptr() {
-    return reinterpret_cast<const void *>(&search_pool_kernel<SUB, MV, RPAD>);
-}
-
-const void *pick_pool_kernel(int sub, int mv, int rpad) {
-#define BANG_P(S, V, P) \
-    if (sub == S && mv == V && rpad == P) return pool_kernel_ptr<S, V, P>();
-    BANG_P(4, 2, 32) BANG_P(4, 2, 64) BANG_P(2, 3, 32) BANG_P(2, 3, 64)
-#undef BANG_P
-    return nullptr;
-}
-
-// Query-pool plan (search_pool_kernel): CTA-shared codebook + Q slots.
-bool plan_pool(bang_index *ix, int64_t nq, int t, int flags, Plan &pl) {
-    const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
-    const int sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
-    if (!sub || ix->R > 64 || (flags & (BANG_EXACT_DISTANCE | BANG_TABLE_GLOBAL | BANG_TABLE_SMEM |
-                                        BANG_CODEBOOK_SMEM | BANG_DEBUG_GENERIC | BANG_WARP_PER_QUERY)))
-        return false;
-    const int rpad = ix->R <= 32 ? 32 : 64;
-    int off = 0;
-    auto take = [&](int64_t bytes) { const int o = off; off += (int)align_up(bytes, 16); return o; };
-    pl.off_q = take(4LL * ix->dim);
-    pl.off_wl = take(8LL * t);
-    pl.off_nk = take(8LL * rpad);
-    pl.off_sk = take(8LL * rpad);
-    pl.off_fid = take(4LL * rpad);
-    pl.off_alive = take(rpad);
-    pl.off_acc = take(128);  // PoolCtl
-    pl.off_vis = take(t);
-    pl.off_sum = take(4LL * pl.sum_words);
-    pl.off_tab = off;
-    pl.per_warp = off;  // bytes per slot
-    pl.shared_bytes = (int)align_up((int64_t)256 * ix->dim * 4, 16) + (int)sizeof(PoolCta);
-    const int q = (int)std::min<int64_t>(kPoolMaxSlots, (ix->max_smem - pl.shared_bytes) / pl.per_warp);
-    if (q < 8) return false;  // too few queries per SM to beat the table kernels
-    const void *kp = pick_pool_kernel(sub, mv, rpad);
-    if (!kp) return false;
-    pl.pool_kernel = true;
-    pl.variant = kAdcSmemCodebook;
-    pl.sub = sub;
-    pl.mv = mv;
-    pl.npl = rpad / 32;
-    pl.pool_slots = q;
-    pl.nt = kPoolThreads;
-    pl.warps = kPoolThreads / 32;
-    pl.smem = pl.shared_bytes + q * pl.per_warp;
-    pl.ctas = (int)std::min<int64_t>(ix->sm_count, std::max<int64_t>(1, ceil_div(nq, q)));
-    pl.slots = pl.ctas * q;
-    pl.rr_ctas = (int)std::min<int64_t>(4LL * ix->sm_count, std::max<int64_t>(1, ceil_div(nq, 8)));
-    return true;
-}
-
-const void *pick_kernel(int npl, int sub, int mv) {
-#define BANG_K(N, S, V) \
-    if (npl == N && sub == S && mv == V) return kernel_ptr<N, S, V>();
-    BANG_K(1, 0, 0) BANG_K(2, 0, 0) BANG_K(4, 0, 0)
-    BANG_K(1, 4, 2) BANG_K(2, 4, 2) BANG_K(4, 4, 2)
-    BANG_K(1, 2, 3) BANG_K(2, 2, 3) BANG_K(4, 2, 3)
-    BANG_K(1, 0, 2) BANG_K(2, 0, 2) BANG_K(4, 0, 2)
-    BANG_K(1, 0, 3) BANG_K(2, 0, 3) BANG_K(4, 0, 3)
-#undef BANG_K
-    return nullptr;
-}
-
+// Kernel + shared-memory layout for one search pass.  Kernel choice
+// (bang_options.kernel, BANG_KERNEL_AUTO by default):
+//   exact distances, the HBM table, the shared codebook or BANG_KERNEL_WARP
+//     -> search_kernel (one warp per query, every ADC data flow);
+//   16-byte code rows (m = 32 or 48) with the per-query smem table
+//     -> search_pf_kernel when the codes exceed L2 and R > 32 (its prefetch
+//        warps hide the HBM gathers; measured slower when the codes are
+//        L2-resident), else search_cta_kernel;
+//   anything else -> search_kernel.
 bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, Plan &pl) {
+    const bang_options &o = ix->opts;
     const int Rpad = std::max(32, (int)align_up(ix->R, 32));
     pl.npl = Rpad <= 32 ? 1 : (Rpad <= 64 ? 2 : 4);
     if (ix->R > 128) return fail(BANG_E_PARAM, "degree bound R=%d exceeds 128", ix->R);
     const bool exact = flags & BANG_EXACT_DISTANCE;
     const int64_t cb_bytes = (int64_t)256 * ix->dim * 4;
-    // per-warp shared memory: query, worklist keys, sorted/unsorted new
-    // keys, fresh ids, partial ADC sums, alive list, visited flags, Bloom
-    // summary (one bit per u32 filter word)
     const int rpad = pl.npl * 32;
     pl.bloom_stride = align_up(ceil_div(z, 32), 4);
     pl.sum_words = (int)ceil_div(pl.bloom_stride, 32);
+    const int mv = (ix->m % 16 == 0 && ix->m / 16 >= 2 && ix->m / 16 <= 3) ? ix->m / 16 : 0;
+    const int vsub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
+    const int64_t tab_bytes = (int64_t)ix->m * 256 * 4;
+    const bool forced_generic = exact || (flags & (BANG_TABLE_GLOBAL | BANG_CODEBOOK_SMEM)) ||
+                                o.kernel == BANG_KERNEL_WARP;
+    if ((o.kernel == BANG_KERNEL_CTA || o.kernel == BANG_KERNEL_PF) && (forced_generic || mv == 0))
+        return fail(BANG_E_PARAM, "the CTA kernels need m = 32 or 48 with the smem table (m=%d, flags=%d)", ix->m,
+                    flags);
+    // ---- one CTA per query (search_cta_kernel / search_pf_kernel)
+    if (!forced_generic && mv > 0) {
+        pl.variant = kAdcSmemTable;
+        pl.sub = vsub;
+        pl.mv = mv;
+        pl.nt = 2 * rpad;
+        const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
+        pl.pfw = o.pf_warps == 1 || o.pf_warps == 2 ? o.pf_warps : (t <= 4 * (pl.nt - 64) ? 2 : 1);
+        const bool pf_ok = !ix->row_hdr && pl.nt >= 128 && t <= 4 * (pl.nt - 32 * pl.pfw) &&
+                           pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, false);
+        if (o.kernel == BANG_KERNEL_PF && !pf_ok)
+            return fail(BANG_E_PARAM, "search_pf_kernel needs an HBM graph, 32 < R <= 128 and t <= %d (t=%d)",
+                        4 * (pl.nt - 32 * pl.pfw), t);
+        const bool pf = o.kernel == BANG_KERNEL_PF || (o.kernel == BANG_KERNEL_AUTO && pf_auto && pf_ok);
+        if (!pf && t > 4 * 2 * rpad)
+            return fail(BANG_E_PARAM, "t=%d exceeds the CTA kernel's worklist limit %d", t, 8 * rpad);
+        pl.kernel = pf ? kKPf : kKCta;
+        int off = 0;
+        auto take = [&](int64_t bytes) { const int o_ = off; off += (int)align_up(bytes, 16); return o_; };
+        pl.off_q = take(4LL * ix->dim);
+        pl.off_wl = take(8LL * t);
+        pl.off_sk = take(8LL * rpad);
+        pl.off_nk = take(8LL * rpad);
+        pl.off_fid = take(4LL * rpad);
+        pl.off_alive = take(rpad);
+        pl.off_acc = take(256);  // CtaMisc / PfMisc
+        pl.off_vis = take(t);
+        // search_pf_kernel clears its filter per query and reads every probe's
+        // word: no summary (its 1.5 KB hold the staged code rows instead)
+        pl.off_sum = pf ? 0 : take(4LL * pl.sum_words);
+        pl.off_tab = take(tab_bytes);
+        if (ix->row_hdr && !pf) pl.off_row = take(4LL * (rpad + 4));
+        if (pf) {
+            // prefetched slots (u32) + pre-state flags (u8)
+            pl.off_dup = take(5LL * pl.nt);
+            // the next row's code rows, staged by the prefetch warps when they fit
+            // the residency search_pf_kernel's launch bounds target (4 CTAs of
+            // 128 threads at m = 48, 6 at m = 32)
+            const int64_t code_bytes = (int64_t)rpad * 16 * pl.mv;
+            const int64_t budget =
+                (int64_t)ix->smem_per_sm / std::max(1, (pl.mv == 3 ? 512 : 768) / pl.nt) - 1024;
+            pl.pf_stage = o.pf_stage != 0 && off + align_up(code_bytes, 16) <= budget;
+            if (pl.pf_stage) pl.off_code = take(code_bytes);
+        }
+        pl.per_warp = off;  // bytes per CTA
+        pl.shared_bytes = 0;
+        pl.warps = pl.nt / 32;
+        pl.smem = pl.per_warp;
+        if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
+        pl.fn = pf ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
+                   : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
+        if (!pl.fn) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
+        CU(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.fn, pl.nt, pl.smem));
+        if (per_sm < 1) return fail(BANG_E_CUDA, "search CTA cannot be resident");
+        pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, nq));
+        pl.slots = pl.ctas;
+        return BANG_OK;
+    }
+    // ---- one warp per query (search_kernel).  Per-warp shared memory: query,
+    // worklist keys, sorted/unsorted new keys, fresh ids, partial ADC sums,
+    // alive list, visited flags, Bloom summary (one bit per u32 filter word)
+    pl.kernel = kKGeneric;
     pl.off_q = 0;
     pl.off_wl = (int)align_up((int64_t)ix->dim * 4, 16);
     pl.off_nk = pl.off_wl + (int)align_up((int64_t)t * 8, 16);
@@ -335,8 +259,6 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     pl.off_vis = pl.off_alive + (int)align_up(rpad, 16);
     pl.off_sum = pl.off_vis + (int)align_up(t, 16);
     pl.per_warp = pl.off_sum + (int)align_up((int64_t)pl.sum_words * 4, 16);
-    const int mv = (ix->m % 16 == 0 && ix->m / 16 >= 2 && ix->m / 16 <= 3) ? ix->m / 16 : 0;
-    const int64_t tab_bytes = (int64_t)ix->m * 256 * 4;
     const int64_t cb_shared = align_up(cb_bytes + 8LL * ix->m, 16);
     if (exact) {
         pl.variant = kAdcExact;
@@ -357,124 +279,72 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     } else {
         pl.variant = kAdcGlobalTable;
     }
-    if ((flags & BANG_QUERY_POOL) && !(flags & BANG_NO_POOL)) {
-        if (plan_pool(ix, nq, t, flags, pl)) {
-            CU(cudaFuncSetAttribute(pick_pool_kernel(pl.sub, pl.mv, pl.npl * 32),
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-            return BANG_OK;
-        }
-        return fail(BANG_E_PARAM, "the query-pool kernel does not support this index/flags (m=%d, sub=%d, R=%d)",
-                    ix->m, ix->uniform_sub, ix->R);
-    }
     pl.off_tab = pl.per_warp;
     if (pl.variant == kAdcSmemTable) pl.per_warp += (int)tab_bytes;
-    if (pl.variant == kAdcSmemCodebook) {
-        pl.shared_bytes = (int)cb_shared;
-        pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
-        pl.mv = pl.sub ? mv : 0;
-    } else if (pl.variant == kAdcSmemTable) {
-        pl.shared_bytes = 0;
-        pl.sub = (ix->uniform_sub == 4 && mv == 2) ? 4 : (ix->uniform_sub == 2 && mv == 3) ? 2 : 0;
-        pl.cta_kernel = mv > 0 && !(flags & (BANG_DEBUG_GENERIC | BANG_WARP_PER_QUERY)) &&
-                        t <= 4 * 2 * rpad;
-        pl.tab_kernel = mv > 0 && !pl.cta_kernel && !(flags & BANG_DEBUG_GENERIC);
-        pl.mv = (pl.sub || pl.tab_kernel || pl.cta_kernel) ? mv : 0;
-    } else {
-        pl.shared_bytes = 0;
-        pl.sub = 0;
-        pl.mv = pl.variant == kAdcGlobalTable ? mv : 0;
-    }
-    if (pl.cta_kernel) {
-        // one CTA per query: 2 threads per neighbour slot; CTA-private layout
-        pl.nt = 2 * rpad;
-        int off = 0;
-        auto take = [&](int64_t bytes) { const int o = off; off += (int)align_up(bytes, 16); return o; };
-        pl.fat_kernel = ix->fat && !(flags & BANG_NO_FAT) && pl.sub && pick_fat_kernel(pl.nt, pl.sub, pl.mv);
-        pl.pipe_kernel = !pl.fat_kernel && (flags & BANG_PIPELINE_ROWS);
-        // one-hop-ahead prefetch of the next row by dedicated warps (graph in
-        // HBM).  It pays when the next row's loads miss L2 -- codes larger than
-        // L2 (C3: 480 MB); with L2-resident codes (C2: 32 MB) the prefetch warps
-        // cost more than they hide (-13%).  BANG_PF=1/0 forces it on/off.
-        const char *pf = getenv("BANG_PF");
-        const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
-        // prefetch warps: two halve the per-lane hashing of the next row (C3:
-        // 765K vs 739K QPS) while two warps still cover sort + merge at
-        // t <= 4*(nt-64); BANG_PF_WARPS=1/2 forces the count
-        const char *pfw = getenv("BANG_PF_WARPS");
-        pl.pfw = pfw ? (*pfw == '2' ? 2 : 1) : (t <= 4 * (pl.nt - 64) ? 2 : 1);
-        pl.pf_kernel = !pl.fat_kernel && !pl.pipe_kernel && !ix->row_hdr &&
-                       (pf ? *pf == '1' : pf_auto) &&
-                       pl.nt >= 128 && t <= 4 * (pl.nt - 32 * pl.pfw) && pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw);
-        const char *pr = getenv("BANG_PF_RED");
-        pl.pf_red = pl.pf_kernel && pr && *pr == '1';
-        pl.off_q = take(4LL * ix->dim);
-        pl.off_wl = take(8LL * t);
-        pl.off_sk = take(8LL * rpad);
-        pl.off_nk = take(8LL * rpad);
-        pl.off_fid = take(4LL * rpad);
-        pl.off_alive = take(rpad);
-        pl.off_acc = take(256);  // CtaMisc
-        pl.off_vis = take(t);
-        // search_pf_kernel clears its filter per query and reads every probe's
-        // word: no summary (its 1.5 KB hold the staged code rows instead)
-        pl.off_sum = pl.pf_kernel ? 0 : take(4LL * pl.sum_words);
-        pl.off_tab = take(tab_bytes);
-        if (ix->row_hdr && !pl.fat_kernel && !pl.pipe_kernel) pl.off_row = take(4LL * (rpad + 4));
-        if (pl.fat_kernel) {
-            pl.off_alive = take(2LL * rpad);            // replay records (flags per probe half)
-            pl.off_dup = take(4LL * kDupSlots + rpad);  // slot-sharing table + truly-fresh bytes
-        }
-        if (pl.pf_kernel) {
-            // prefetched slots (u32) + pre-state flags (u8) [+ slot-sharing table]
-            pl.off_dup = take(5LL * pl.nt + (pl.pf_red ? 4LL * kDupSlots : 0));
-            // the next row's code rows, staged by the prefetch warps when they fit
-            const int64_t code_bytes = (int64_t)rpad * 16 * pl.mv;
-            const char *st = getenv("BANG_PF_STAGE");
-            // (the residency search_pf_kernel's launch bounds target: 4 CTAs of
-            // 128 threads at m = 48, 6 at m = 32)
-            const int64_t budget = (int64_t)ix->smem_per_sm / std::max(1, (pl.mv == 3 ? 512 : 768) / pl.nt) - 1024;
-            pl.pf_stage = !(st && *st == '0') && pl.mv > 0 && off + align_up(code_bytes, 16) <= budget;
-            if (pl.pf_stage) pl.off_code = take(code_bytes);
-        }
-        pl.per_warp = off;  // bytes per CTA
-        pl.shared_bytes = 0;
-        pl.warps = pl.nt / 32;
-        pl.smem = pl.per_warp;
-        if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
-        const void *kc = pl.fat_kernel    ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
-                         : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                         : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
-                                          : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
-        if (!kc) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
-        CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
-        int per_sm = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kc, pl.nt, pl.smem));
-        if (per_sm < 1) return fail(BANG_E_CUDA, "search CTA cannot be resident");
-        pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, nq));
-        pl.slots = pl.ctas;
-        return BANG_OK;
-    }
+    pl.shared_bytes = pl.variant == kAdcSmemCodebook ? (int)cb_shared : 0;
+    pl.sub = (pl.variant == kAdcSmemCodebook || pl.variant == kAdcSmemTable) ? vsub : 0;
+    pl.mv = (pl.sub || pl.variant == kAdcGlobalTable) ? mv : 0;
     int64_t w = (ix->max_smem - pl.shared_bytes) / pl.per_warp;
     if (w < 1) return fail(BANG_E_PARAM, "t=%d needs %d B of shared memory per query", t, pl.per_warp);
-    pl.warps = (int)std::min<int64_t>((pl.tab_kernel ? 256 : kMaxSearchThreads) / 32, w);
+    pl.warps = (int)std::min<int64_t>(kMaxSearchThreads / 32, w);
     pl.smem = pl.shared_bytes + pl.warps * pl.per_warp;
-    const void *kfn = pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv) : pick_kernel(pl.npl, pl.sub, pl.mv);
-    if (!kfn) return fail(BANG_E_STATE, "no kernel instance for npl=%d sub=%d mv=%d", pl.npl, pl.sub, pl.mv);
-    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+    pl.fn = pick_kernel(pl.npl, pl.sub, pl.mv);
+    if (!pl.fn) return fail(BANG_E_STATE, "no kernel instance for npl=%d sub=%d mv=%d", pl.npl, pl.sub, pl.mv);
+    CU(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
     int per_sm = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pl.warps * 32, pl.smem));
-    if (per_sm < 1) {
-        // registers: shrink the CTA until it fits
-        while (pl.warps > 1 && per_sm < 1) {
-            pl.warps = pl.warps / 2;
-            pl.smem = pl.shared_bytes + pl.warps * pl.per_warp;
-            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, pl.warps * 32, pl.smem));
-        }
-        if (per_sm < 1) return fail(BANG_E_CUDA, "search kernel cannot be resident");
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.fn, pl.warps * 32, pl.smem));
+    while (pl.warps > 1 && per_sm < 1) {  // registers: shrink the CTA until it fits
+        pl.warps = pl.warps / 2;
+        pl.smem = pl.shared_bytes + pl.warps * pl.per_warp;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.fn, pl.warps * 32, pl.smem));
     }
+    if (per_sm < 1) return fail(BANG_E_CUDA, "search kernel cannot be resident");
     pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, ceil_div(nq, pl.warps)));
     pl.slots = pl.ctas * pl.warps;
     return BANG_OK;
+}
+
+// L2 persistence of the Bloom filters: the device-wide carve-out is shared by
+// every index on the device; the first index to set it records the previous
+// limit, the last one destroyed resets the persisting lines and restores it.
+struct PersistState {
+    int users = 0;
+    size_t prev_limit = 0;
+    size_t limit = 0;
+};
+std::mutex g_persist_mu;
+std::map<int, PersistState> g_persist;
+
+bang_status persist_acquire(bang_index *ix, size_t want) {
+    std::lock_guard<std::mutex> lk(g_persist_mu);
+    PersistState &ps = g_persist[ix->device];
+    if (!ix->persist_user) {
+        if (ps.users == 0) {
+            CU(cudaDeviceGetLimit(&ps.prev_limit, cudaLimitPersistingL2CacheSize));
+            ps.limit = ps.prev_limit;
+        }
+        ++ps.users;
+        ix->persist_user = true;
+    }
+    if (want > ps.limit) {
+        CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+        ps.limit = want;
+    }
+    ix->persist_set = ps.limit;
+    return BANG_OK;
+}
+
+void persist_release(bang_index *ix) {
+    if (!ix->persist_user) return;
+    std::lock_guard<std::mutex> lk(g_persist_mu);
+    PersistState &ps = g_persist[ix->device];
+    ix->persist_user = false;
+    if (--ps.users == 0) {
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, ps.prev_limit);
+        cudaGetLastError();
+        g_persist.erase(ix->device);
+    }
 }
 
 // Enqueue one search pass.  Outputs are indexed by query id; log rows by
@@ -484,16 +354,19 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
                         float *d_dists, int32_t *d_iters, uint8_t *d_short, int32_t *d_log,
                         int64_t log_cap, const float *d_table, cudaStream_t st) {
     if (ix->bloom.reserve((size_t)pl.slots * pl.bloom_stride)) return BANG_E_OOM;
-    if (ix->rr.reserve((size_t)(pl.pool_kernel ? pl.rr_ctas * 8 : pl.slots) * log_cap)) return BANG_E_OOM;
+    if (ix->rr.reserve((size_t)pl.slots * log_cap)) return BANG_E_OOM;
+    const bang_options &o = ix->opts;
+    const bool cta = pl.kernel == kKCta || pl.kernel == kKPf;
     SearchParams p{};
     p.codes = ix->codes;
+    p.code_stride = ix->code_stride;
     p.centroids = ix->centroids;
     p.sub_off = ix->d_sub_off;
     p.sub_size = ix->d_sub_size;
     p.table = d_table;
     p.adj = ix->adj;
     p.adj_stride = ix->adj_stride;
-    p.row_hdr = ix->row_hdr && pl.cta_kernel && !pl.fat_kernel && !pl.pipe_kernel ? 1 : 0;
+    p.row_hdr = ix->row_hdr && pl.kernel == kKCta ? 1 : 0;
     p.off_row = pl.off_row;
     p.deg = ix->deg;
     p.vectors = ix->vectors;
@@ -526,8 +399,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.adc_variant = pl.variant;
     p.rerank = (flags & BANG_RERANK) ? 1 : 0;
     p.debug = (flags & BANG_DEBUG_CHECKS) ? 1 : 0;
-    p.profile = (flags & BANG_PROFILE_PHASES) ? 1 : 0;
-    if (p.profile && getenv("BANG_PF_BREAKDOWN")) p.profile = 2;  // pf kernel: slots 4/5 = warp 0's stages
+    p.profile = (flags & BANG_PROFILE_PHASES) ? (o.profile == 2 ? 2 : 1) : 0;
     p.smem_shared_bytes = pl.shared_bytes;
     p.per_warp_bytes = pl.per_warp;
     p.off_q = pl.off_q;
@@ -541,77 +413,45 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_sum = pl.off_sum;
     p.sum_words = pl.sum_words;
     p.off_tab = pl.off_tab;
-    p.pool_slots = pl.pool_slots;
-    p.fat = ix->fat;
-    p.fat_stride = ix->fat_stride;
-    p.fat_code_off = ix->fat_code_off;
     p.off_dup = pl.off_dup;
-    {
-        const char *bc = getenv("BANG_BLOOM_CLEAR");
-        p.bloom_clear = !(bc && *bc == '0');
-        const char *pl2 = getenv("BANG_PF_L2");
-        p.pf_l2 = pl2 ? atoi(pl2) : 2;
-        p.pf_red = pl.pf_red;
-        p.pf_stage = pl.pf_stage;
-        p.off_code = pl.off_code;
-        const char *ps = getenv("BANG_PF_SPEC");
-        p.pf_spec = !(ps && *ps == '0');
-        const char *ps2 = getenv("BANG_PF_SPEC2");
-        p.pf_spec2 = ps2 && *ps2 == '1';  // measured neutral at C3 (795K vs 797K)
-        const char *pea = getenv("BANG_PF_EARLY");
-        p.pf_early = !pl.pf_red && !(pea && *pea == '0');
-        const char *pe = getenv("BANG_PF_EAGER");
-        p.pf_eager = pe && *pe == '1';
-    }
+    p.bloom_clear = o.bloom_clear != 0;
+    p.pf_stage = pl.pf_stage;
+    p.off_code = pl.off_code;
+    p.pf_spec = o.pf_spec != 0;
+    p.pf_early = o.pf_early != 0;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
-    if (pl.pool_kernel) {
-        void *pargs[] = {&p};
-        CU(cudaLaunchKernel(pick_pool_kernel(pl.sub, pl.mv, pl.npl * 32), dim3(pl.ctas), dim3(kPoolThreads), pargs,
-                            (size_t)pl.smem, st));
-        if (p.rerank)
-            rerank_log_kernel<<<pl.rr_ctas, 256, (size_t)8 * ix->dim * sizeof(float), st>>>(p);
-        CU(cudaGetLastError());
-        return BANG_OK;
-    }
-    const void *kfn = pl.fat_kernel  ? pick_fat_kernel(pl.nt, pl.sub, pl.mv)
-                      : pl.pipe_kernel ? pick_pipe_kernel(pl.nt, pl.sub, pl.mv)
-                      : pl.pf_kernel   ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
-                      : pl.cta_kernel  ? pick_cta_kernel(pl.nt, pl.sub, pl.mv, p.row_hdr != 0)
-                      : pl.tab_kernel ? pick_tab_kernel(pl.npl, pl.sub, pl.mv)
-                                      : pick_kernel(pl.npl, pl.sub, pl.mv);
     void *args[] = {&p};
+    const dim3 grid(pl.ctas), block(cta ? pl.nt : pl.warps * 32);
     // The per-slot Bloom filters (C2: 888 x 50 KB, C3: 592 x 50 KB) are the
     // search's only re-read random working set; the code/adjacency/vector
     // gathers stream past them.  Mark the filters L2-persisting for this
-    // launch (BANG_NO_L2_PERSIST=1 disables) so Bloom words stay L2 hits.
-    const char *nopersist = getenv("BANG_NO_L2_PERSIST");
+    // launch (bang_options.l2_persist) so Bloom words stay L2 hits.
     const size_t bloom_bytes = (size_t)pl.slots * pl.bloom_stride * 4;
-    if (ix->persist_max > 0 && !(nopersist && *nopersist == '1')) {
-        const size_t win = std::min<size_t>(bloom_bytes, (size_t)ix->persist_max);
-        if (ix->persist_set != win) {
-            CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, win));
-            ix->persist_set = win;
-        }
+    if (ix->persist_max > 0 && o.l2_persist) {
+        bang_status s = persist_acquire(ix, std::min<size_t>(bloom_bytes, (size_t)ix->persist_max));
+        if (s) return s;
+        const size_t win = std::min<size_t>(bloom_bytes, (size_t)ix->window_max);
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(pl.ctas);
-        cfg.blockDim = dim3(pl.warps * 32);
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
         cfg.dynamicSmemBytes = (size_t)pl.smem;
         cfg.stream = st;
         cudaLaunchAttribute attr{};
         attr.id = cudaLaunchAttributeAccessPolicyWindow;
         attr.val.accessPolicyWindow.base_ptr = ix->bloom.p;
-        attr.val.accessPolicyWindow.num_bytes = std::min<size_t>(bloom_bytes, (size_t)ix->window_max);
-        attr.val.accessPolicyWindow.hitRatio = 1.0f;
+        attr.val.accessPolicyWindow.num_bytes = win;
+        // a window larger than the carve-out would thrash the persisting set
+        attr.val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)ix->persist_set / (double)win));
         attr.val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         attr.val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cfg.attrs = &attr;
         cfg.numAttrs = 1;
-        CU(cudaLaunchKernelExC(&cfg, kfn, args));
+        CU(cudaLaunchKernelExC(&cfg, pl.fn, args));
         return BANG_OK;
     }
-    CU(cudaLaunchKernel(kfn, dim3(pl.ctas), dim3(pl.warps * 32), args, (size_t)pl.smem, st));
+    CU(cudaLaunchKernel(pl.fn, grid, block, args, (size_t)pl.smem, st));
     return BANG_OK;
 }
 
@@ -670,11 +510,12 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
     CU(cudaEventRecord(ix->ev[2], st));
     ix->stats = bang_search_stats{};
     ix->stats.queries = nq;
+    ix->k_last = k;
     ix->stats.slots = pl.slots;
     ix->stats.warps_per_cta = pl.warps;
     ix->stats.ctas = pl.ctas;
     ix->stats.adc_variant = pl.variant;
-    ix->stats.kernel = pl.pool_kernel ? 4 : pl.fat_kernel ? 3 : pl.pipe_kernel ? 5 : pl.pf_kernel ? 6 : pl.cta_kernel ? 2 : pl.tab_kernel ? 1 : 0;
+    ix->stats.kernel = pl.kernel;
     ix->last_nq = nq;
     ix->last_log_cap = cap;
     ix->last_has_table = d_table != nullptr;
@@ -699,14 +540,13 @@ bang_status collect(bang_index *ix, unsigned long long *ctr) {
     S.kernel_ms = ms_total;
     S.table_ms = ix->last_has_table ? ms_table : 0.f;
     const int64_t elem = ix->vec_dtype == BANG_VEC_F32 ? 4 : 1;
-    // adjacency rows + degree, two Bloom words
-    // read per probe and written per admission, code rows of the admitted,
-    // re-rank vectors, queries in, results + visit logs out.
-    // (fat rows: the code rows of every expanded neighbour arrive with the ids)
-    const int64_t code_rows = S.kernel == 3 ? S.probes : S.fresh;
-    S.algorithmic_bytes = S.iterations * 8 + S.probes * 4 + S.probes * 8 + S.fresh * 8 +
-                          code_rows * ix->m + S.rerank_cands * ix->dim * elem +
-                          S.queries * (ix->dim * 4 + 16);
+    // SURVEY.md 8(d) "whole search" bytes: per query-iteration
+    // the adjacency row + degree (4R + 4), per probe its id and two u64 Bloom
+    // words (20), per fresh neighbour its code row, id and key (m + 12); per
+    // re-rank candidate its vector + id + key; per query the query in and
+    // the k results out
+    S.algorithmic_bytes = S.iterations * (4LL * ix->R + 4) + S.probes * 20 + S.fresh * (ix->m + 12) +
+                          S.rerank_cands * (ix->dim * elem + 12) + S.queries * (ix->dim * 4 + 8LL * ix->k_last);
     S.adc_bytes = S.fresh * (ix->m + 12);
     for (int i = 0; i < 8; ++i) S.phase_cycles[i] = (int64_t)ctr[kCtrPhase0 + i];
     ix->pending = false;
@@ -796,9 +636,18 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
     CUX(cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking));
     for (auto &e : ix->ev) CUX(cudaEventCreate(&e));
     const size_t elem = vec_dtype == BANG_VEC_F32 ? 4 : 1;
+    bang_options_default(&ix->opts);
+    // m = 48 code rows are padded to 64 bytes: a gathered row is then one
+    // aligned 64-byte DRAM burst instead of straddling two
+    ix->code_stride = m == 48 ? 64 : m;
     if (m > 0) {
-        CUX(cudaMalloc(&ix->codes, (size_t)n * m));
-        CUX(cudaMemcpy(ix->codes, codes, (size_t)n * m, cudaMemcpyHostToDevice));
+        CUX(cudaMalloc(&ix->codes, (size_t)n * ix->code_stride));
+        if (ix->code_stride == m) {
+            CUX(cudaMemcpy(ix->codes, codes, (size_t)n * m, cudaMemcpyHostToDevice));
+        } else {
+            CUX(cudaMemset(ix->codes, 0, (size_t)n * ix->code_stride));
+            CUX(cudaMemcpy2D(ix->codes, ix->code_stride, codes, m, m, n, cudaMemcpyHostToDevice));
+        }
         CUX(cudaMalloc(&ix->centroids, (size_t)256 * dim * 4));
         CUX(cudaMemcpy(ix->centroids, centroids, (size_t)256 * dim * 4, cudaMemcpyHostToDevice));
         CUX(cudaMalloc(&ix->d_sub_off, sizeof(int32_t) * m));
@@ -841,24 +690,6 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
         CUX(cudaMemcpy(ix->adj, adjacency, adj_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->deg, degrees, deg_bytes, cudaMemcpyHostToDevice));
         CUX(cudaMemcpy(ix->vectors, vectors, vec_bytes, cudaMemcpyHostToDevice));
-        // fat rows for search_fat_kernel: ids + the neighbours' code rows inline
-        // (one coalesced read per hop).  Opt-in (BANG_FAT_ROWS=1): measured
-        // slower than separate code rows at C2/C3 (profiles/r01/fat_rows.txt)
-        const char *fatenv = getenv("BANG_FAT_ROWS");
-        if (m > 0 && m % 16 == 0 && m / 16 <= 3 && fatenv && *fatenv == '1') {
-            ix->fat_code_off = (int32_t)align_up(4LL * R, 16);
-            ix->fat_stride = align_up(ix->fat_code_off + (int64_t)R * m, 16);
-            if (cudaMalloc(&ix->fat, (size_t)n * ix->fat_stride) == cudaSuccess) {
-                const int64_t blocks = std::min<int64_t>(ceil_div(n * 32, 256), (int64_t)ix->sm_count * 16);
-                build_fat_rows_kernel<<<(unsigned)blocks, 256, 0, ix->stream>>>(
-                    ix->adj, ix->deg, ix->codes, n, R, m, ix->fat_code_off, ix->fat_stride, ix->fat);
-                CUX(cudaGetLastError());
-                CUX(cudaStreamSynchronize(ix->stream));
-            } else {
-                cudaGetLastError();
-                ix->fat = nullptr;
-            }
-        }
     } else {
         return cleanup_fail(fail(BANG_E_PARAM, "unknown graph placement %d", graph_placement));
     }
@@ -871,8 +702,8 @@ void bang_index_destroy(bang_index *ix) {
     if (!ix) return;
     cudaSetDevice(ix->device);
     if (ix->stream) cudaStreamSynchronize(ix->stream);
+    persist_release(ix);
     cudaFree(ix->codes);
-    cudaFree(ix->fat);
     cudaFree(ix->centroids);
     cudaFree(ix->d_sub_off);
     cudaFree(ix->d_sub_size);
@@ -1083,7 +914,57 @@ bang_status bang_last_search_stats(const bang_index *ix, bang_search_stats *out)
     return BANG_OK;
 }
 
+void bang_options_default(bang_options *o) {
+    if (!o) return;
+    *o = bang_options{};
+    o->kernel = BANG_KERNEL_AUTO;
+    o->pf_warps = 0;
+    o->pf_stage = 1;
+    o->pf_early = 1;
+    o->pf_spec = 1;
+    o->bloom_clear = 1;
+    o->l2_persist = 1;
+    o->profile = 0;
+}
+
+bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {
+    if (!ix || !o) return fail(BANG_E_STATE, "null argument");
+    if (o->kernel < BANG_KERNEL_AUTO || o->kernel > BANG_KERNEL_PF)
+        return fail(BANG_E_PARAM, "unknown kernel %d", o->kernel);
+    if (o->pf_warps < 0 || o->pf_warps > 2) return fail(BANG_E_PARAM, "pf_warps must be 0, 1 or 2");
+    ix->opts = *o;
+    return BANG_OK;
+}
+
+bang_status bang_index_get_options(const bang_index *ix, bang_options *o) {
+    if (!ix || !o) return fail(BANG_E_STATE, "null argument");
+    *o = ix->opts;
+    return BANG_OK;
+}
+
+int32_t bang_index_code_stride(const bang_index *ix) { return ix ? ix->code_stride : 0; }
+
 // ------------------------------------------------------------ per-kernel entries
+
+bang_status bang_pq_table(bang_index *ix, const float *queries, int64_t nq, float *out) {
+    if (!ix) return fail(BANG_E_STATE, "GraphSearcher is not fitted (null index)");
+    if (ix->m < 1) return fail(BANG_E_PARAM, "index has no PQ codebook");
+    if (nq < 0) return fail(BANG_E_PARAM, "nq must be >= 0");
+    if (nq == 0) return BANG_OK;
+    if (!queries || !out) return fail(BANG_E_PARAM, "NULL queries/out");
+    CU(cudaSetDevice(ix->device));
+    cudaStream_t st = ix->stream;
+    bang_status s;
+    if ((s = ix->q.reserve((size_t)nq * ix->dim))) return s;
+    if ((s = ix->table.reserve((size_t)nq * ix->m * 256))) return s;
+    CU(cudaMemcpyAsync(ix->q.p, queries, sizeof(float) * nq * ix->dim, cudaMemcpyHostToDevice, st));
+    pq_table_kernel<<<(unsigned)nq, 256, ix->dim * sizeof(float), st>>>(ix->centroids, ix->d_sub_off, ix->d_sub_size,
+                                                                       ix->m, ix->dim, ix->q.p, ix->table.p);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, ix->table.p, sizeof(float) * nq * ix->m * 256, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return BANG_OK;
+}
 
 bang_status bang_pq_table_device(const float *d_centroids, const int32_t *sub_sizes, int32_t m, int32_t dim,
                                  const float *d_queries, int64_t nq, float *d_out, void *stream) {
@@ -1147,28 +1028,22 @@ bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_
     cudaStream_t st = stream ? reinterpret_cast<cudaStream_t>(stream) : ix->stream;
     const int mv = (ix->m % 16 == 0) ? ix->m / 16 : 0;
     const int sub = ix->uniform_sub;
-    // BANG_ADC_PAIRS=lanes: code rows straight into registers, sums carried
-    // across the row's lanes (adc_pairs_lanes_kernel); default: smem-staged rows
-    const char *var = std::getenv("BANG_ADC_PAIRS");
     const bool vec = (sub == 4 && mv == 2) || (sub == 2 && mv == 3);
-    const bool lanes = vec && var && std::strcmp(var, "lanes") == 0;
-    // table + query (+ per-warp double-buffered code-row stages, staged vector path)
+    // table + query (+ per-warp double-buffered code-row stages, vector path)
     const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + align_up(ix->dim, 4)) +
-                        (vec && !lanes ? (size_t)8 * 2 * 32 * ix->m : 0);
+                        (vec ? (size_t)8 * 2 * 32 * ix->m : 0);
     if (smem > (size_t)ix->max_smem) return fail(BANG_E_PARAM, "table of m=%d does not fit in shared memory", ix->m);
     auto launch = [&](const void *fn) -> bang_status {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
         const int64_t grid = std::min<int64_t>(nq, (int64_t)ix->sm_count * std::max(1, per_sm));
-        int m = ix->m, dim = ix->dim;
+        int m = ix->m, dim = ix->dim, cs = ix->code_stride;
         void *args[] = {&ix->centroids, &ix->d_sub_off, &ix->d_sub_size, &m, &dim, &d_queries, &nq,
-                        &d_off, &d_ids, &ix->codes, &d_keys};
+                        &d_off, &d_ids, &ix->codes, &cs, &d_keys};
         CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st));
         return BANG_OK;
     };
-    if (lanes && sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_lanes_kernel<4, 2>));
-    if (lanes && sub == 2 && mv == 3) return launch(reinterpret_cast<const void *>(&adc_pairs_lanes_kernel<2, 3>));
     if (sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<4, 2>));
     if (sub == 2 && mv == 3) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<2, 3>));
     return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<0, 0>));

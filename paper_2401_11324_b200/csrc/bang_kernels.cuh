@@ -71,38 +71,27 @@ struct SearchParams {
     int32_t smem_shared_bytes, per_warp_bytes;
     int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
-    int32_t pool_slots; // search_pool_kernel: query slots per CTA
-    // search_fat_kernel: rows [ids R x i32 | pad | codes R x m] (bang_search_fat.cuh)
-    const uint8_t *fat;
-    int64_t fat_stride;
-    int32_t fat_code_off, off_dup;
+    int32_t off_dup;    // search_pf_kernel: prefetched slots + pre-state flags
     // adjacency row i starts at adj + i * adj_stride.  row_hdr: host-mapped
     // rows carry a 16-byte header [deg, 0, 0, 0] at adj - 4 so one coalesced
     // read fetches degree + ids (search_cta_kernel stages it at off_row)
     int64_t adj_stride;
     int32_t row_hdr, off_row;
     // search_cta_kernel: clear the slot's filter with whole-line stores at
-    // query start (else words are zeroed on first touch; BANG_BLOOM_CLEAR=0)
+    // query start (else words are zeroed on first touch; bang_options.bloom_clear)
     int32_t bloom_clear;
-    // search_pf_kernel: L2 prefetch of the next row's code rows (0 none,
-    // 1 cp.async.bulk.prefetch, 2 prefetch.global.L2; BANG_PF_L2)
-    int32_t pf_l2;
-    // search_pf_kernel: fire-and-forget Bloom sets, slot sharing found by
-    // warp 0 ahead of time (BANG_PF_RED=0: fetch-or results)
-    int32_t pf_red;
     // search_pf_kernel: L2 prefetch of the candidate winners' rows (the head
-    // at expand time, each warp's best fresh neighbour; BANG_PF_SPEC=0 off)
+    // at expand time, each warp's best fresh neighbour; bang_options.pf_spec)
     int32_t pf_spec;
-    int32_t pf_eager;  // (measurement only) wait for the fetch-or before the ADC
     // search_pf_kernel: the prefetch warps stage the next row's code rows at
     // off_code (rpad x 16*MV bytes) instead of prefetching them into L2
     int32_t pf_stage, off_code;
-    // search_pf_kernel: two-hop speculative L2 prefetch of the head's
-    // neighbours' code rows (BANG_PF_SPEC2)
-    int32_t pf_spec2;
     // search_pf_kernel: the prefetch warps perform the next row's Bloom sets
-    // (fetch-or) one iteration ahead (BANG_PF_EARLY)
+    // (fetch-or) one iteration ahead (bang_options.pf_early)
     int32_t pf_early;
+    // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
+    // one DRAM burst per gathered row)
+    int32_t code_stride;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -111,9 +100,6 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     return t;
 }
 
-__global__ void record_t0_kernel(unsigned long long *counters) {
-    counters[kCtrT0] = globaltimer_ns();
-}
 
 // Top-k of unique keys keys[0, L) (global, written by this warp) into
 // out_ids/out_dists; k rounds of a warp-wide min above the last pick.
@@ -189,7 +175,7 @@ __device__ __forceinline__ int adc_survivors(const SearchParams &p, const float 
                 j = s0 == 0 ? a : s_alive[a];
                 const uint32_t node = s_fid[j];
                 float acc = s0 == 0 ? 0.0f : s_acc[j];
-                const uint64_t c8 = load_code8<(MV > 0)>(p.codes + (int64_t)node * m, s0, ns);
+                const uint64_t c8 = load_code8<(MV > 0)>(p.codes + (int64_t)node * p.code_stride, s0, ns);
                 if (p.adc_variant == kAdcSmemCodebook)
                     acc = adc_cb_stage<SUB>(acc, s_cb, s_q, s_off, s_sz, s0, ns, c8);
                 else
@@ -278,7 +264,7 @@ __device__ __forceinline__ int adc_fast_path(const SearchParams &p, const float 
             if (a < n_alive) {
                 node = s_fid[a];
                 acc = s_acc[a];
-                const uint4 cv = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)node * p.m) + st);
+                const uint4 cv = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)node * p.code_stride) + st);
                 acc = cb ? adc_cb_stage16<SUB>(acc, s_cb, s_q, 16 * st, cv) : adc_tab_stage16(acc, trow, 16 * st, cv);
                 if (last) {
                     key = pack_key(acc, node);
@@ -397,11 +383,11 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
         float d0 = 0.f;
         if (lane == 0) {
             if (p.adc_variant == kAdcSmemCodebook)
-                d0 = adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)p.medoid * p.m);
+                d0 = adc_codebook<SUB, MV>(s_cb, s_q, s_off, s_sz, p.m, p.codes + (int64_t)p.medoid * p.code_stride);
             else if (p.adc_variant == kAdcGlobalTable)
-                d0 = adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)p.medoid * p.m);
+                d0 = adc_table<MV>(p.table + qid * (int64_t)p.m * 256, p.m, p.codes + (int64_t)p.medoid * p.code_stride);
             else if (p.adc_variant == kAdcSmemTable)
-                d0 = adc_table<MV>(s_tab, p.m, p.codes + (int64_t)p.medoid * p.m);
+                d0 = adc_table<MV>(s_tab, p.m, p.codes + (int64_t)p.medoid * p.code_stride);
             else
                 d0 = exact_sq_dist(p.vectors, p.vec_dtype, p.dim, p.medoid, s_q);
             s_wl[0] = pack_key(d0, (uint32_t)p.medoid);
@@ -454,7 +440,7 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
 #pragma unroll
                 for (int k = 0; k < NPL; ++k)
                     if (lane + 32 * k < deg)
-                        c0[k] = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)ids[k] * p.m));
+                        c0[k] = __ldg(reinterpret_cast<const uint4 *>(p.codes + (int64_t)ids[k] * p.code_stride));
             }
             BANG_PHASE(1)
             BloomRow<NPL> br;
@@ -591,426 +577,4 @@ __global__ void __launch_bounds__(kMaxSearchThreads, 1) search_kernel(const Sear
     }
 }
 
-// -------------------------------------------------------------------------
-// Kernel 1 -- build_pq_dist_table (pq.py:284-319).  One CTA per query,
-// thread c = centroid c, subspaces in order; each subspace row (1 KB) is
-// written coalesced.  Exact f32 op order, no FMA.
-// -------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) pq_table_kernel(const float *__restrict__ centroids,
-                                                       const int32_t *__restrict__ sub_off,
-                                                       const int32_t *__restrict__ sub_size,
-                                                       int m, int dim,
-                                                       const float *__restrict__ queries,
-                                                       float *__restrict__ out) {
-    extern __shared__ float s_qt[];
-    const int64_t q = blockIdx.x;
-    for (int j = threadIdx.x; j < dim; j += blockDim.x) s_qt[j] = __ldg(queries + q * dim + j);
-    __syncthreads();
-    const int c = threadIdx.x;
-    float *o = out + q * (int64_t)m * 256;
-    for (int s = 0; s < m; ++s) {
-        const int off = __ldg(sub_off + s), sz = __ldg(sub_size + s);
-        const float *cc = centroids + (int64_t)off * 256 + (int64_t)c * sz;
-        float d = __fsub_rn(s_qt[off], __ldg(cc));
-        float acc = __fmul_rn(d, d);
-        for (int j = 1; j < sz; ++j) {
-            d = __fsub_rn(s_qt[off + j], __ldg(cc + j));
-            acc = __fadd_rn(acc, __fmul_rn(d, d));
-        }
-        __stcs(o + s * 256 + c, acc);
-    }
-}
-
-// -------------------------------------------------------------------------
-// Kernel 2 -- BloomFilterBank.filter_and_set (bloom.py:124-163): one warp
-// per filter row, the row's probes processed 32 at a time in order.
-// -------------------------------------------------------------------------
-__global__ void bloom_bank_kernel(uint32_t *bits, int64_t count, int64_t words32, BloomGeom g,
-                                  const int64_t *__restrict__ row_off,
-                                  const uint32_t *__restrict__ ids, uint8_t *fresh) {
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (row >= count) return;
-    const int lane = (int)lane_id();
-    uint32_t *b = bits + row * words32;
-    const int64_t lo = row_off[row], hi = row_off[row + 1];
-    for (int64_t base = lo; base < hi; base += 32) {
-        const int cnt = (int)min((int64_t)32, hi - base);
-        uint32_t id[1] = {lane < cnt ? ids[base + lane] : 0u};
-        bool fr[1];
-        bloom_test_and_set<1>(b, nullptr, g, id, cnt, fr);
-        if (lane < cnt) fresh[base + lane] = fr[0] ? 1 : 0;
-    }
-}
-
-// -------------------------------------------------------------------------
-// Kernel 3 -- ADC over (query row, node) pairs (engine.py:99-105) with the
-// key pack of engine.py:195-199.  One thread per pair, code row gathered as
-// 16-byte vectors when m % 16 == 0.
-// -------------------------------------------------------------------------
-template <int MV>
-__global__ void adc_kernel(const float *__restrict__ table, int m,
-                           const uint8_t *__restrict__ codes, const int64_t *__restrict__ qrows,
-                           const uint32_t *__restrict__ ids, int64_t n, float *dists,
-                           uint64_t *keys) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t node = __ldg(ids + i);
-    const float d = adc_table<MV>(table + __ldg(qrows + i) * (int64_t)m * 256, m,
-                                  codes + (int64_t)node * m);
-    if (dists) dists[i] = d;
-    if (keys) keys[i] = pack_key(d, node);
-}
-
-// -------------------------------------------------------------------------
-// Kernel 4a -- merge_sort_rows (kernels.py:94-109).  One CTA per row; each
-// element's stable rank (#less + #equal-before) is its output slot, which
-// yields exactly the ascending row for any width.
-// -------------------------------------------------------------------------
-__global__ void sort_rows_kernel(uint64_t *keys, int w) {
-    extern __shared__ uint64_t s_row[];
-    uint64_t *row = keys + (int64_t)blockIdx.x * w;
-    for (int i = threadIdx.x; i < w; i += blockDim.x) s_row[i] = row[i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < w; i += blockDim.x) {
-        const uint64_t v = s_row[i];
-        int r = 0;
-        for (int j = 0; j < w; ++j) {
-            const uint64_t x = s_row[j];
-            r += (x < v) || (x == v && j < i);
-        }
-        row[r] = v;
-    }
-}
-
-// Kernel 4b -- merge_rows (kernels.py:68-87): a_i -> i + #{b < a_i};
-// b_j -> j + #{a <= b_j} (the reference's rank merge, a first on ties).
-__global__ void merge_rows_kernel(const uint64_t *__restrict__ a, const uint8_t *__restrict__ a_pay,
-                                  int wa, const uint64_t *__restrict__ b, int wb, uint64_t *out,
-                                  uint8_t *out_pay) {
-    const int64_t r = blockIdx.x;
-    const uint64_t *ar = a + r * wa, *br = b + r * wb;
-    uint64_t *o = out + r * (int64_t)(wa + wb);
-    uint8_t *op = out_pay ? out_pay + r * (int64_t)(wa + wb) : nullptr;
-    for (int i = threadIdx.x; i < wa; i += blockDim.x) {
-        const int pos = i + lower_bound_u64(br, wb, ar[i]);
-        o[pos] = ar[i];
-        if (op) op[pos] = a_pay ? a_pay[r * wa + i] : 0;
-    }
-    for (int j = threadIdx.x; j < wb; j += blockDim.x) {
-        const int pos = j + upper_bound_u64(ar, wa, br[j]);
-        o[pos] = br[j];
-        if (op) op[pos] = 0;
-    }
-}
-
-// -------------------------------------------------------------------------
-// Kernel 4 (engine step) -- eager pick + sort + merge + truncate + converge
-// (engine.py:201-217) per worklist row, one warp per row, through the same
-// survivor filter / sort_keys / merge_sorted the fused kernel runs.
-// Shared memory per warp: wl keys (t), sorted + unsorted new keys (w each),
-// visited flags (t).
-// -------------------------------------------------------------------------
-__global__ void worklist_update_kernel(uint64_t *wl_keys, uint8_t *wl_vis, int64_t rows, int t,
-                                       const uint64_t *__restrict__ new_keys, int w,
-                                       uint64_t *winner, uint8_t *done) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-    const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (row >= rows) return;
-    const int a_wl = (t * 8 + 15) & ~15, a_k = (w * 8 + 15) & ~15;
-    const int per_warp = a_wl + 2 * a_k + ((t + 15) & ~15);
-    unsigned char *base = smem + (size_t)warp * per_warp;
-    uint64_t *s_wl = reinterpret_cast<uint64_t *>(base);
-    uint64_t *s_sk = reinterpret_cast<uint64_t *>(base + a_wl);
-    uint64_t *s_nk = reinterpret_cast<uint64_t *>(base + a_wl + a_k);
-    uint8_t *s_vis = base + a_wl + 2 * a_k;
-    uint64_t *gw = wl_keys + row * t;
-    uint8_t *gv = wl_vis + row * t;
-    int cnt = 0;
-    for (int b = 0; b < t; b += 32) {
-        const int i = b + lane;
-        bool real = false;
-        if (i < t) {
-            s_wl[i] = gw[i];
-            s_vis[i] = gv[i];
-            real = gw[i] != kSentinel;
-        }
-        cnt += __popc(__ballot_sync(kFull, real));
-    }
-    __syncwarp();
-    // survivors: non-sentinel new keys that can rank below t
-    const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
-    int n = 0;
-    uint64_t best_all = kSentinel;
-    for (int b = 0; b < w; b += 32) {
-        const int i = b + lane;
-        const uint64_t v = i < w ? new_keys[row * w + i] : kSentinel;
-        best_all = v < best_all ? v : best_all;
-        const bool keep = v != kSentinel && v < thr;
-        const unsigned m = __ballot_sync(kFull, keep);
-        if (keep) s_nk[n + __popc(m & ((1u << lane) - 1u))] = v;
-        n += __popc(m);
-    }
-    best_all = warp_min_u64(best_all);
-    __syncwarp();
-    sort_keys(s_nk, n, s_sk);
-    const int hpos = first_unvisited(s_vis, 0, cnt);
-    const uint64_t head = hpos < cnt ? s_wl[hpos] : kSentinel;
-    const uint64_t win = best_all < head ? best_all : head;  // engine.py:202-204 (all new keys)
-    int first = 0;
-    cnt = merge_sorted(s_wl, s_vis, cnt, t, s_sk, n, &first);
-    const int upos = first_unvisited(s_vis, 0, cnt);
-    for (int i = lane; i < t; i += 32) {
-        gw[i] = i < cnt ? s_wl[i] : kSentinel;
-        gv[i] = i < cnt ? s_vis[i] : 0;
-    }
-    if (lane == 0) {
-        winner[row] = win;
-        done[row] = upos >= cnt ? 1 : 0;
-    }
-}
-
-// -------------------------------------------------------------------------
-// Kernel 5 -- re-rank (engine.py:244-262): one warp per query over its
-// candidates; keys staged in `scratch` (same CSR layout).
-// -------------------------------------------------------------------------
-__global__ void rerank_kernel(const void *vectors, int dtype, int dim,
-                              const float *__restrict__ queries, int64_t nq,
-                              const int64_t *__restrict__ off, const int32_t *__restrict__ cand,
-                              uint64_t *scratch, int k, int32_t *out_ids, float *out_dists,
-                              uint8_t *out_short) {
-    extern __shared__ float s_qr[];
-    const int warp = threadIdx.x >> 5, lane = (int)lane_id();
-    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (q >= nq) return;
-    float *sq = s_qr + (size_t)warp * dim;
-    for (int j = lane; j < dim; j += 32) sq[j] = queries[q * dim + j];
-    __syncwarp();
-    const int64_t lo = off[q], L = off[q + 1] - lo;
-    for (int64_t i = lane; i < L; i += 32) {
-        const uint32_t node = (uint32_t)cand[lo + i];
-        scratch[lo + i] = pack_key(exact_sq_dist(vectors, dtype, dim, node, sq), node);
-    }
-    __threadfence_block();
-    __syncwarp();
-    warp_topk_write(scratch + lo, L, k, out_ids + q * k, out_dists + q * k);
-    if (lane == 0) out_short[q] = L < k;
-}
-
-// Visit-log compaction: row r of a (rows, cap) log -> CSR at out + off[dst(r)],
-// dst(r) = map ? map[r] : r.  One warp per row.
-__global__ void compact_logs_kernel(const int32_t *__restrict__ log, int64_t cap, int64_t rows,
-                                    const int32_t *__restrict__ map, const int64_t *__restrict__ off,
-                                    const uint8_t *__restrict__ skip, int32_t *out) {
-    const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (r >= rows) return;
-    const int64_t q = map ? map[r] : r;
-    if (skip && skip[q]) return;
-    const int64_t lo = off[q], len = off[q + 1] - lo;
-    for (int64_t i = lane_id(); i < len; i += 32) out[lo + i] = log[r * cap + i];
-}
-
-// exact_sq_dists (engine.py:48-51), row-paired, one thread per row.
-__global__ void exact_dists_kernel(const void *points, int dtype, int dim,
-                                   const float *__restrict__ queries, int64_t n, float *out) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    out[i] = exact_sq_dist(points, dtype, dim, i, queries + i * dim);
-}
-
-}  // namespace bang
-
-namespace bang {
-// -------------------------------------------------------------------------
-// Kernel 3 over a query-grouped pair list (north_star kernel 3; SURVEY.md
-// 8(d) "a standalone ADC launch over all (query, neighbour) pairs"): one CTA
-// per query builds the query's table in shared memory (kernel 1, pq.py:284-296
-// op order), then every pair of that query gathers its PQ code row with
-// 16-byte loads and sums the table entries sequentially in f32
-// (engine.py:99-105).  keys[i] = f32bits << 32 | ids[i].  Pairs of query q are
-// ids[off[q], off[q+1]).  SUB/MV > 0: uniform subspaces of width SUB and
-// m = 16*MV (vector path); 0: generic.
-// -------------------------------------------------------------------------
-template <int SUB, int MV>
-__global__ void __launch_bounds__(256) adc_pairs_kernel(const float *__restrict__ centroids,
-                                                        const int32_t *__restrict__ sub_off,
-                                                        const int32_t *__restrict__ sub_size, int m,
-                                                        int dim, const float *__restrict__ queries,
-                                                        int64_t nq, const int64_t *__restrict__ off,
-                                                        const uint32_t *__restrict__ ids,
-                                                        const uint8_t *__restrict__ codes,
-                                                        uint64_t *__restrict__ keys) {
-    extern __shared__ __align__(16) float s_tab[];  // m*256 table, then the query
-    float *s_q = s_tab + (size_t)m * 256;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        for (int i = tid; i < dim; i += nt) s_q[i] = __ldg(queries + q * dim + i);
-        __syncthreads();
-        for (int idx = tid; idx < m * 256; idx += nt) {
-            const int s = idx >> 8, c = idx & 255;
-            float e;
-            if constexpr (SUB == 4) {
-                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
-                                 __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
-            } else if constexpr (SUB == 2) {
-                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
-                                 __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
-            } else {
-                const int o = __ldg(sub_off + s), sz = __ldg(sub_size + s);
-                e = table_entry(s_q + o, centroids + (int64_t)o * 256 + c * sz, sz);
-            }
-            s_tab[idx] = e;
-        }
-        __syncthreads();
-        const int64_t lo = off[q], hi = off[q + 1];
-        if constexpr (MV > 0) {
-            // Per warp, rounds of 32 pairs: the 32 code rows are copied into
-            // the warp's smem stage by cp.async with MV consecutive lanes per
-            // row (coalesced 16-byte pieces, no registers held), double
-            // buffered so round r+1's rows are in flight while round r sums.
-            constexpr int M = 16 * MV;
-            const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-            uint8_t *stage = reinterpret_cast<uint8_t *>(s_q + ((dim + 3) & ~3)) + (size_t)warp * 2 * 32 * M;
-            const int64_t nround = (hi - lo + 31) / 32;
-            auto issue = [&](int64_t r, int buf) -> uint32_t {
-                const int64_t base = lo + r * 32;
-                const uint32_t my = base + lane < hi ? __ldg(ids + base + lane) : 0u;
-#pragma unroll
-                for (int v = 0; v < MV; ++v) {
-                    const int ci = v * 32 + lane, row = ci / MV, part = ci - row * MV;
-                    const uint32_t rid = __shfl_sync(kFull, my, row);
-                    if (base + row < hi)
-                        __pipeline_memcpy_async(stage + (size_t)buf * 32 * M + ci * 16,
-                                                codes + (int64_t)rid * M + part * 16, 16);
-                }
-                __pipeline_commit();
-                return my;
-            };
-            int64_t r = warp;
-            uint32_t cur = r < nround ? issue(r, 0) : 0u;
-            for (int k = 0; r < nround; ++k, r += nw) {
-                const int64_t rn = r + nw;
-                uint32_t nxt = 0u;
-                if (rn < nround) {
-                    nxt = issue(rn, (k + 1) & 1);
-                    __pipeline_wait_prior(1);
-                } else {
-                    __pipeline_wait_prior(0);
-                }
-                __syncwarp();
-                const int64_t i = lo + r * 32 + lane;
-                if (i < hi) {
-                    const uint4 *row = reinterpret_cast<const uint4 *>(stage + (size_t)(k & 1) * 32 * M + lane * M);
-                    float a = 0.0f;
-#pragma unroll
-                    for (int v = 0; v < MV; ++v) a = adc_tab_stage16(a, s_tab, 16 * v, row[v]);
-                    keys[i] = pack_key(a, cur);
-                }
-                __syncwarp();  // this buffer is refilled two rounds later
-                cur = nxt;
-            }
-        } else {
-            for (int64_t i = lo + tid; i < hi; i += nt) {
-                const uint32_t node = __ldg(ids + i);
-                keys[i] = pack_key(adc_table<0>(s_tab, m, codes + (int64_t)node * m), node);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// -------------------------------------------------------------------------
-// Kernel 3 over query-grouped pairs, lane-pipelined variant: code rows go
-// straight from L2/HBM into registers (no shared-memory staging), MV lanes
-// per row with one coalesced 16-byte load each.  Lane (j, p) owns subspaces
-// [16p, 16p+16) of row j, so the exact sequential f32 sum (engine.py:102-104)
-// is carried across the row's lanes: the partial sum moves one lane up per
-// round (shfl), and lane p works on the batch loaded p rounds before lane 0's.
-// Every lane keeps its own 16-byte piece in a register ring of S = D + MV
-// slots (D = rounds of load lead), so no piece is ever re-read or shuffled.
-// Same arguments and results as adc_pairs_kernel.
-// -------------------------------------------------------------------------
-template <int SUB, int MV>
-__global__ void __launch_bounds__(256, 4) adc_pairs_lanes_kernel(const float *__restrict__ centroids,
-                                                              const int32_t *__restrict__ sub_off,
-                                                              const int32_t *__restrict__ sub_size, int m,
-                                                              int dim, const float *__restrict__ queries,
-                                                              int64_t nq, const int64_t *__restrict__ off,
-                                                              const uint32_t *__restrict__ ids,
-                                                              const uint8_t *__restrict__ codes,
-                                                              uint64_t *__restrict__ keys) {
-    static_assert(SUB == 2 || SUB == 4, "vector path only");
-    constexpr int M = 16 * MV;      // code row bytes
-    constexpr int RPW = 32 / MV;    // rows per warp round
-    constexpr int D = 2;            // load lead, rounds
-    constexpr int S = D + MV;       // register ring slots
-    extern __shared__ __align__(16) float s_tab[];  // m*256 table, then the query
-    float *s_q = s_tab + (size_t)m * 256;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    const int j = lane / MV, p = lane - j * MV;
-    const bool row_lane = j < RPW;
-    const float *tp = s_tab + p * 16 * 256;  // this lane's 16 subspace tables
-    for (int64_t q = blockIdx.x; q < nq; q += gridDim.x) {
-        for (int i = tid; i < dim; i += nt) s_q[i] = __ldg(queries + q * dim + i);
-        __syncthreads();
-        for (int idx = tid; idx < m * 256; idx += nt) {
-            const int s = idx >> 8, c = idx & 255;
-            float e;
-            if constexpr (SUB == 4)
-                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
-                                 __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
-            else
-                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
-                                 __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
-            s_tab[idx] = e;
-        }
-        __syncthreads();
-        const int64_t lo = off[q];
-        const int npair = (int)(off[q + 1] - lo);
-        // this warp's batches b: rows r(b) = warp*RPW + j + b*nw*RPW of the query's pairs
-        const int nbt = (npair + RPW - 1) / RPW;
-        const int nb = nbt > warp ? (nbt - warp + nw - 1) / nw : 0;
-        const int r0w = warp * RPW + j, rstep = nw * RPW;
-        const uint32_t *qids = ids + lo;
-        uint64_t *qkeys = keys + lo;
-        uint4 ring[S];
-        uint32_t rid[S];
-        auto load = [&](int b, uint4 &cv, uint32_t &id) {
-            const int ri = r0w + b * rstep;
-            if (row_lane && b < nb && ri < npair) {
-                id = __ldg(qids + ri);
-                cv = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)id * M) + p);
-            }
-        };
-#pragma unroll
-        for (int u = 0; u < D; ++u) load(u, ring[u], rid[u]);
-        float acc_in = 0.0f;
-        const int nround = nb + MV - 1;
-        for (int r0 = 0; r0 < nround; r0 += S) {
-#pragma unroll
-            for (int u = 0; u < S; ++u) {
-                const int r = r0 + u;
-                if (r >= nround) break;
-                load(r + D, ring[(u + D) % S], rid[(u + D) % S]);
-                // lane p works on batch r - p, whose piece sits in slot (u - p) mod S
-                uint4 cv = ring[u % S];
-                if constexpr (MV >= 2) if (p == 1) cv = ring[(u + S - 1) % S];
-                if constexpr (MV >= 3) if (p == 2) cv = ring[(u + S - 2) % S];
-                const int b = r - p, ri = r0w + b * rstep;
-                const bool live = row_lane && b >= 0 && b < nb && ri < npair;
-                float acc = p == 0 ? 0.0f : acc_in;
-                if (live) {
-                    const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        acc = __fadd_rn(acc, tp[i * 256 + ((w[i >> 2] >> ((i & 3) * 8)) & 0xFFu)]);
-                    if (p == MV - 1) qkeys[ri] = pack_key(acc, rid[(u + S - (MV - 1)) % S]);
-                }
-                acc_in = __shfl_up_sync(kFull, acc, 1);
-            }
-        }
-        __syncthreads();
-    }
-}
 }  // namespace bang

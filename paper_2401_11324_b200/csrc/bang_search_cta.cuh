@@ -21,26 +21,6 @@
 
 namespace bang {
 
-// in-row slot-sharing table (open addressing over Bloom slot numbers), used
-// by search_fat_kernel and search_pf_kernel
-constexpr uint32_t kDupEmpty = 0xFFFFFFFFu;
-constexpr int kDupSlots = 256;
-
-// Claims slot ps in the row's table; true if another probe of the row already
-// holds it.  *didx = the entry this probe filled (cleared after the row).
-__device__ __forceinline__ bool dup_claim(uint32_t *s_dup, uint32_t ps, int *didx) {
-    uint32_t x = (ps * 0x9E3779B1u) >> 24;
-    for (;;) {
-        const uint32_t old = atomicCAS(s_dup + x, kDupEmpty, ps);
-        if (old == kDupEmpty) {
-            *didx = (int)x;
-            return false;
-        }
-        if (old == ps) return true;
-        x = (x + 1) & (kDupSlots - 1);
-    }
-}
-
 struct CtaMisc {
     unsigned long long wmin[8];  // per-warp survivor minimum
     int wcnt[8];                 // per-warp survivor count
@@ -181,7 +161,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
         }
         __syncthreads();
         if (tid == 0) {  // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125)
-            const uint8_t *row = p.codes + (int64_t)p.medoid * M;
+            const uint8_t *row = p.codes + (int64_t)p.medoid * p.code_stride;
             float acc = 0.0f;
             for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
             s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
@@ -217,7 +197,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_cta_ker
             // ---- this half's code bytes, in flight with the Bloom word
             uint32_t cw[MHW];
             if (valid) {
-                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * M) + h * MHW;
+                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * p.code_stride) + h * MHW;
                 if constexpr (MHW == 4) {
                     const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row));
                     cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;

@@ -46,9 +46,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 __device__ __forceinline__ void named_bar_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void l2_prefetch_bulk(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void l2_prefetch(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");
 }
@@ -76,7 +73,7 @@ __device__ __forceinline__ long long clock_after(int v) {
 template <int NT, int MV, int PFW>
 __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int lane, uint8_t *s_code,
                                        const uint32_t *bits, uint32_t *s_nid, uint32_t *s_nps,
-                                       uint8_t *s_nfl, uint32_t *s_dup, PfMisc *s_m) {
+                                       uint8_t *s_nfl, PfMisc *s_m) {
     constexpr int PL = NT / (64 * PFW);  // neighbour slots per lane (RPAD = NT/2 over PFW warps)
     constexpr int PT = 32 * PFW;         // prefetch threads; lane = index among them
     constexpr int M = 16 * MV;
@@ -104,13 +101,11 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
         ps1[r] = ps2[r] = wd1[r] = wd2[r] = 0u;
         i1[r] = i2[r] = false;
         if (jj < deg) {
-            const uint8_t *crow = p.codes + (int64_t)nid[r] * M;
+            const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
             if (p.pf_stage) {
 #pragma unroll
                 for (int v = 0; v < MV; ++v) __pipeline_memcpy_async(s_code + jj * M + v * 16, crow + v * 16, 16);
-            } else if (p.pf_l2 == 1) {
-                l2_prefetch_bulk(crow, M);
-            } else if (p.pf_l2 == 2) {
+            } else {
                 l2_prefetch(crow);
                 if (((uintptr_t)crow & 31u) + M > 32u) l2_prefetch(crow + M - 1);
             }
@@ -128,28 +123,9 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
         for (int r = 0; r < PL; ++r) x ^= wd1[r] ^ wd2[r];
         s_m->ph[5] += (unsigned long long)(clock_after((int)x) - c0);
     }
-    // slot sharing among the row's probes (exact, open addressing): the later
-    // claimer of a shared slot is flagged; a node's own p1 == p2 is one claim
     bool sh1[PL], sh2[PL];
-    int d1[PL], d2[PL];
 #pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        sh1[r] = sh2[r] = false;
-        d1[r] = d2[r] = -1;
-        if (p.pf_red && lane + PT * r < deg) {
-            sh1[r] = dup_claim(s_dup, ps1[r], &d1[r]);
-            if (ps2[r] != ps1[r]) sh2[r] = dup_claim(s_dup, ps2[r], &d2[r]);
-        }
-    }
-    if (p.pf_red) {
-        if (PFW == 1) __syncwarp();
-        else named_bar_sync(3, PT);
-#pragma unroll
-        for (int r = 0; r < PL; ++r) {
-            if (d1[r] >= 0) s_dup[d1[r]] = kDupEmpty;
-            if (d2[r] >= 0) s_dup[d2[r]] = kDupEmpty;
-        }
-    }
+    for (int r = 0; r < PL; ++r) sh1[r] = sh2[r] = false;
     // early Bloom sets (p.pf_early): the row's presumed-fresh probes set their
     // bits now, one iteration ahead of their test (the test reads the
     // pre-state bits above, and no other row of this query runs in between).
@@ -164,9 +140,10 @@ __device__ __forceinline__ void pf_row(const SearchParams &p, uint32_t w, int la
             const uint32_t b1 = (wd1[r] >> (ps1[r] & 31)) & 1u, b2 = (wd2[r] >> (ps2[r] & 31)) & 1u;
             fr[r] = lane + PT * r < deg && !(b1 && b2);  // (consumes this thread's word loads)
         }
-        // every prefetch warp holds its pre-state words before any set of the
-        // row lands (one warp: program order already guarantees it)
+        // every prefetch lane holds its pre-state words before any set of the
+        // row lands (lanes of one warp are not ordered without the warp barrier)
         if (PFW > 1) named_bar_sync(3, PT);
+        else __syncwarp();
 #pragma unroll
         for (int r = 0; r < PL; ++r) {
             o1[r] = o2[r] = 0u;
@@ -228,7 +205,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     uint8_t *s_code = smem + p.off_code;  // next row's code rows (pf_stage)
     uint32_t *s_nps = reinterpret_cast<uint32_t *>(smem + p.off_dup);
     uint8_t *s_nfl = smem + p.off_dup + 4 * NT;
-    uint32_t *s_dup = reinterpret_cast<uint32_t *>(smem + p.off_dup + 5 * NT);  // warp 0's slot table
     PfMisc *s_m = reinterpret_cast<PfMisc *>(smem + p.off_acc);
     uint32_t *bits = p.bloom + (int64_t)blockIdx.x * p.bloom_stride;
     uint64_t *rr = p.rr_scratch + (int64_t)blockIdx.x * p.log_cap;
@@ -240,8 +216,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
     const bool prof = p.profile && tc == 0;
     if (tc == 0)
         for (int i = 0; i < 8; ++i) s_m->ph[i] = 0;
-    if (p.pf_red)  // the slot-sharing table exists only then
-        for (int i = tid; i < kDupSlots; i += NT) s_dup[i] = kDupEmpty;  // (barrier at the query fetch)
 #define BANG_PF_PHASE(i)                                       \
     if (prof) {                                                \
         const long long now_ = clock64();                      \
@@ -300,12 +274,12 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
         }
         __syncthreads();
         if (tid == 0) {  // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125)
-            const uint8_t *row = p.codes + (int64_t)p.medoid * M;
+            const uint8_t *row = p.codes + (int64_t)p.medoid * p.code_stride;
             float acc = 0.0f;
             for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
             s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
         }
-        if (pfw) pf_row<NT, MV, PFW>(p, (uint32_t)p.medoid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+        if (pfw) pf_row<NT, MV, PFW>(p, (uint32_t)p.medoid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_m);
         int cnt = 1, upos = 0;
         uint32_t u = (uint32_t)p.medoid;
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
@@ -340,16 +314,6 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
 
         for (;;) {
             ++iters;  // u was expanded (logged, marked) before the last barrier
-            // two hops ahead (speculative): if the head wins this iteration,
-            // its neighbours' code rows are the next prefetch's HBM gathers.
-            // Read the head's row now (it was sent towards L2 at expand) and,
-            // after the ADC, ask L2 for those code rows.
-            int32_t spec_nb = -1;
-            // (iteration 1: the prologue's expand is still writing the head)
-            if (p.pf_spec2 && iters > 1 && h == 0 && j < p.R) {
-                const uint64_t hd = s_m->head;
-                if (hd != kSentinel) spec_nb = __ldcg(p.adj + (int64_t)key_id(hd) * p.adj_stride + j);
-            }
             const int deg = s_m->ndeg;
             st_probes += deg;
             const bool valid = j < deg;
@@ -372,7 +336,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 id = s_nid[j];
                 ps = s_nps[tid];
                 fl = s_nfl[tid];
-                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * M) + h * MHW;
+                const uint32_t *row = reinterpret_cast<const uint32_t *>(p.codes + (int64_t)id * p.code_stride) + h * MHW;
                 if constexpr (MHW == 4) {
                     const uint4 v = __ldg(reinterpret_cast<const uint4 *>(row));
                     cw[0] = v.x; cw[1] = v.y; cw[2] = v.z; cw[3] = v.w;
@@ -391,15 +355,11 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
             const uint32_t pps = __shfl_xor_sync(kFull, ps, 1);
             bool fresh = valid && !(mybit && pbit);
             BANG_PF_PHASE(0)  // (phase 1, the zeroing barrier, does not exist here)
-            // pf_red: fire-and-forget sets, in-row slot sharing known from
-            // warp 0's table; else the fetch-or result tells
+            // the fetch-or result tells in-row slot sharing (pf_early: the sets
+            // were performed one iteration ahead by the prefetch warps)
             uint32_t old = 0;
             const bool do_atom = fresh && !(h == 1 && pps == ps);
-            if (do_atom && !p.pf_early) {  // (pf_early: set one iteration ahead by the prefetch warps)
-                if (p.pf_red) atomicOr(bits + (ps >> 5), 1u << (ps & 31));
-                else old = atomicOr(bits + (ps >> 5), 1u << (ps & 31));
-            }
-            if (p.pf_eager) asm volatile("" ::"r"(old));  // A/B: wait for the fetch-or here
+            if (do_atom && !p.pf_early) old = atomicOr(bits + (ps >> 5), 1u << (ps & 31));
             const uint64_t thr = cnt == t ? s_wl[t - 1] : kSentinel;
             uint64_t key = kSentinel;
             bool surv = false;
@@ -433,18 +393,13 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 // Bloom collision check (fetch-or results) folded into the barrier
                 // (the fetch-or result is consumed only here, after the ADC)
                 const bool coll = pass == 0 && do_atom && !mybit &&
-                                  ((p.pf_red || p.pf_early) ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0);
+                                  (p.pf_early ? (fl & 4u) != 0 : (old & (1u << (ps & 31))) != 0);
                 if (lane == 0) {
                     s_m->wmin[warp] = wm;
                     s_m->wcnt[warp] = __popc(sb);
                     s_m->wfresh[warp] = __popc(fb);
                     // this warp's best fresh neighbour may be the next winner
                     if (p.pf_spec && pass == 0 && wm != kSentinel) prefetch_row_l2(p, key_id(wm));
-                }
-                if (pass == 0 && spec_nb >= 0) {  // (adjacency rows are -1 padded)
-                    const uint8_t *crow = p.codes + (int64_t)spec_nb * M;
-                    l2_prefetch(crow);
-                    if (((uintptr_t)crow & 31u) + M > 32u) l2_prefetch(crow + M - 1);
                 }
                 BANG_PF_PHASE(2)
                 const int any_coll = __syncthreads_or(coll);
@@ -487,7 +442,7 @@ __global__ void __launch_bounds__(NT, (MV == 3 ? 512 : 768) / NT) search_pf_kern
                 // ---- one hop ahead: the winner's row while warps PFW.. sort + merge
                 named_bar_arrive(1, NT);
                 const long long c0 = p.profile ? clock64() : 0;
-                if (winner != kSentinel) pf_row<NT, MV, PFW>(p, wid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_dup, s_m);
+                if (winner != kSentinel) pf_row<NT, MV, PFW>(p, wid, tid, s_code, bits, s_nid, s_nps, s_nfl, s_m);
                 if (p.profile && tid == 0) s_m->ph[1] += (unsigned long long)(clock_after(s_nfl[0]) - c0);
             } else {
                 named_bar_sync(1, NT);  // all survivors published

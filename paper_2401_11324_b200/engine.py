@@ -204,6 +204,34 @@ class DeviceIndex:
         _lib.check(_lib.lib().bang_last_search_stats(self.handle, ctypes.byref(s)))
         return s.as_dict()
 
+    def options(self) -> dict:
+        o = _lib.Options()
+        _lib.check(_lib.lib().bang_index_get_options(self.handle, ctypes.byref(o)), "bang_index_get_options")
+        return o.as_dict()
+
+    def set_options(self, kernel: str = "auto", **tuning) -> None:
+        """bang_index_set_options: kernel in _lib.KERNEL_CHOICES plus the
+        bang_options tuning fields (pf_warps, pf_stage, pf_early, pf_spec,
+        bloom_clear, l2_persist, profile); unnamed fields keep their defaults."""
+        if kernel not in _lib.KERNEL_CHOICES:
+            raise ParameterError(f"unknown kernel {kernel!r}; expected one of {sorted(_lib.KERNEL_CHOICES)}")
+        o = _lib.Options()
+        L = _lib.lib()
+        L.bang_options_default(ctypes.byref(o))
+        o.kernel = _lib.KERNEL_CHOICES[kernel]
+        for name, value in tuning.items():
+            if name not in o.as_dict() or name == "kernel":
+                raise ParameterError(f"unknown search option {name!r}")
+            setattr(o, name, int(value))
+        _lib.check(L.bang_index_set_options(self.handle, ctypes.byref(o)), "bang_index_set_options")
+
+    def pq_table(self, queries: np.ndarray) -> np.ndarray:
+        """bang_pq_table: kernel 1 on host buffers (pq.py:299-319)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        out = np.empty((q.shape[0], self.m, 256), np.float32)
+        _lib.check(_lib.lib().bang_pq_table(self.handle, _lib.ptr(q), q.shape[0], _lib.ptr(out)), "bang_pq_table")
+        return out
+
 
 def exact_sq_dists(points, queries) -> np.ndarray:
     """engine.py:48-51 on the GPU: row-paired squared L2, f64 sums -> f32."""
@@ -304,13 +332,22 @@ class GraphSearcher(BaseEstimator):
         else:
             codebook, codes = None, None
         placement = _lib.GRAPH_HOST_MAPPED if self.mode == "pipelined" else _lib.GRAPH_HBM
+        # ``device`` (not a constructor parameter): the GPU this replica uses
+        # (sharding.ShardedSearcher sets one per replica); default BANG_DEVICE/LOCAL_RANK.
+        # The new index is created before the old one is released, so a failed
+        # re-fit (e.g. out of memory) leaves the previous index usable.
+        new_index = DeviceIndex(graph, base, codebook, codes, placement, device=getattr(self, "device", None))
+        opts = getattr(self, "_kernel_options", None)
+        if opts is not None:
+            try:
+                new_index.set_options(**opts)
+            except Exception:
+                new_index.close()
+                raise
         old = getattr(self, "index_", None)
+        self.index_ = new_index
         if old is not None:
             old.close()
-        # ``device`` (not a constructor parameter): the GPU this replica uses
-        # (sharding.ShardedSearcher sets one per replica); default BANG_DEVICE/LOCAL_RANK
-        self.index_ = DeviceIndex(graph, base, codebook, codes, placement,
-                                  device=getattr(self, "device", None))
         self.host_ = IndexHost(graph, base)
         self.graph_ = graph
         self.codebook_ = codebook
@@ -319,17 +356,7 @@ class GraphSearcher(BaseEstimator):
         return self
 
     _ADC_FLAGS = {"auto": 0, "smem-table": _lib.TABLE_SMEM, "codebook": _lib.CODEBOOK_SMEM,
-                  "hbm-table": _lib.TABLE_GLOBAL,
-                  # the smem table through the generic kernel (cross-check of the specialised one)
-                  "smem-table-generic": _lib.TABLE_SMEM | _lib.DEBUG_GENERIC,
-                  # the smem table with one warp (not one CTA) per query
-                  "smem-table-warp": _lib.TABLE_SMEM | _lib.WARP_PER_QUERY,
-                  # lockstep query pool per CTA with the CTA-shared codebook
-                  "pool": _lib.QUERY_POOL,
-                  # CTA per query without the fat-row layout (ids and codes read separately)
-                  "smem-table-nofat": _lib.TABLE_SMEM | _lib.NO_FAT,
-                  # CTA per query with the next row's code/Bloom loads issued during the merge
-                  "pipelined-rows": _lib.TABLE_SMEM | _lib.PIPELINE_ROWS}
+                  "hbm-table": _lib.TABLE_GLOBAL}
 
     def set_adc_variant(self, name: str) -> "GraphSearcher":
         """Pick the ADC data flow (results are identical for all of them):
@@ -339,6 +366,15 @@ class GraphSearcher(BaseEstimator):
         if name not in self._ADC_FLAGS:
             raise ParameterError(f"unknown ADC variant {name!r}")
         self._adc_variant = name
+        return self
+
+    def set_kernel(self, kernel: str = "auto", **tuning) -> "GraphSearcher":
+        """Pick the search kernel ("auto", "warp", "cta", "pf") and its tuning
+        (bang_options in include/bang.h).  Results are identical for every
+        choice; this only moves work between warps and memory levels."""
+        self._kernel_options = dict(kernel=kernel, **tuning)
+        if getattr(self, "index_", None) is not None:
+            self.index_.set_options(**self._kernel_options)
         return self
 
     def _flags(self) -> int:

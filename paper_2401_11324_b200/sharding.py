@@ -85,7 +85,26 @@ class ShardedSearcher:
         self._pool = ThreadPoolExecutor(max_workers=len(self.devices))
 
     def fit(self, X, y=None, graph=None, codebook=None, codes=None) -> "ShardedSearcher":
-        # uploads are independent per device: run them concurrently too
+        # Missing artifacts are built ONCE (on this process's device) and the
+        # same objects go to every replica: the builders' GPU reductions are
+        # not bitwise deterministic, so per-replica builds could differ and
+        # break the equal-to-one-GPU guarantee.
+        data = getattr(X, "data", X)
+        p = self.params
+        if graph is None:
+            from .tools.graph_build import build_graph
+            graph = build_graph(np.asarray(data), degree_bound=p.get("degree_bound", 64),
+                                build_worklist=p.get("build_worklist", 200), sigma=p.get("sigma", 1.2),
+                                seed=p.get("seed", 0))
+        if p.get("mode", "pipelined") != "exact_distance":
+            if codebook is None:
+                from .tools.pq_train import train_codebook
+                codebook = train_codebook(np.asarray(data), m=p.get("m", 74), iters=p.get("pq_iters", 25),
+                                          seed=p.get("seed", 0))
+            if codes is None:
+                from .tools.pq_train import encode
+                codes = encode(np.asarray(data), codebook)
+        # uploads are independent per device: run them concurrently
         futs = [self._pool.submit(s.fit, X, y, graph, codebook, codes) for s in self.searchers]
         for f in futs:
             f.result()
@@ -94,6 +113,11 @@ class ShardedSearcher:
     def set_adc_variant(self, name: str) -> "ShardedSearcher":
         for s in self.searchers:
             s.set_adc_variant(name)
+        return self
+
+    def set_kernel(self, kernel: str = "auto", **tuning) -> "ShardedSearcher":
+        for s in self.searchers:
+            s.set_kernel(kernel, **tuning)
         return self
 
     def set_params(self, **params) -> "ShardedSearcher":

@@ -119,13 +119,11 @@ def test_kernel3_adc_vectorised_code_rows():
             assert np.array_equal(got, want[rows == q])
 
 
-@pytest.mark.parametrize("variant", ["staged", "lanes"])
 @pytest.mark.parametrize("d,m", [(128, 32), (96, 48), (20, 8)])
-def test_kernel3_adc_pairs_query_grouped(d, m, variant, monkeypatch):
+def test_kernel3_adc_pairs_query_grouped(d, m):
     """bang_adc_pairs_device (table built in shared memory per query) equals
-    the oracle's table + sequential ADC, including empty pair ranges; both
-    code-row data flows (smem-staged rows, lane-pipelined register rows)."""
-    monkeypatch.setenv("BANG_ADC_PAIRS", variant)
+    the oracle's table + sequential ADC, including empty pair ranges (m = 48
+    code rows are 64-byte padded on the device)."""
     import torch
     from paper_2401_11324_b200 import _lib
     from paper_2401_11324_b200.tools.pq_train import encode, train_codebook
@@ -137,6 +135,7 @@ def test_kernel3_adc_pairs_query_grouped(d, m, variant, monkeypatch):
     graph = B.GraphIndex(np.zeros((n, 4), np.int32), np.zeros(n, np.int32), 0, 4)
     s = B.GraphSearcher(k=1, t=4, mode="in_memory")
     s.fit(base, graph=graph, codebook=cb, codes=B.CompressedVectors(codes))
+    assert _lib.lib().bang_index_code_stride(s.index_.handle) == (64 if m == 48 else m)
     nq = 37
     q = rng.normal(size=(nq, d)).astype(np.float32)
     counts = rng.integers(0, 700, size=nq)
@@ -155,6 +154,22 @@ def test_kernel3_adc_pairs_query_grouped(d, m, variant, monkeypatch):
                                                 _lib.ptr(dk), None))
     torch.cuda.synchronize()
     assert np.array_equal(dk.cpu().numpy().view(np.uint64), np.asarray(want, np.uint64))
+
+
+def test_kernel1_pq_table_host_entry():
+    """bang_pq_table (host buffers, the handle's codebook) equals the
+    reference's build_pq_dist_table (pq.py:299-319)."""
+    g = gu.load("pq_table.npz")
+    for tag in "cd":
+        q = g[f"{tag}_q"]
+        cents = gu.split_centroids(g[f"{tag}_centroids"], g[f"{tag}_sizes"])
+        cb = B.PQCodebook(dim=q.shape[1], subspace_sizes=[int(s) for s in g[f"{tag}_sizes"]], centroids=cents)
+        n = 64
+        codes = B.CompressedVectors(np.zeros((n, cb.m), np.uint8))
+        graph = B.GraphIndex(np.zeros((n, 4), np.int32), np.zeros(n, np.int32), 0, 4)
+        s = B.GraphSearcher(k=1, t=4, mode="in_memory").fit(np.zeros((n, q.shape[1]), np.float32), graph=graph,
+                                                           codebook=cb, codes=codes)
+        assert np.array_equal(s.index_.pq_table(q), g[f"{tag}_table"]), tag
 
 
 def test_kernel4_sort_and_merge_rows():
@@ -330,6 +345,21 @@ def _random_case(seed, n, d, R, m, nq, dtype=np.float32):
     return base, q, graph, cb, encode(base, cb)
 
 
+# (ADC flags, kernel option) combinations: every data flow of every kernel
+_VARIANTS = [("auto", "auto"), ("smem-table", "auto"), ("smem-table", "warp"), ("codebook", "auto"),
+             ("hbm-table", "auto"), ("smem-table", "cta")]
+
+
+def _oracle_search(q, graph, cb, codes, base, t, z=399_887, rerank=True, k=10):
+    return O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
+                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
+                    k=k, t=t, bloom_entries=z, rerank=rerank, threads=8)
+
+
+def _same_as_oracle(res, want):
+    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+
+
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
     (1, 20_000, 128, 64, 32, 64, np.uint8),   # C2 shape at reduced n: sub=4, m=32 fast path
     (2, 20_000, 96, 64, 48, 48, np.float32),  # C3 shape at reduced n: sub=2, m=48 fast path
@@ -339,26 +369,25 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=399_887, threads=8)
-    variants = ["auto", "smem-table", "smem-table-warp", "smem-table-generic", "codebook", "hbm-table",
-                "smem-table-nofat"]
-    if m in (32, 48) and R <= 64:
-        variants.append("pool")
-        s.set_adc_variant("auto").search(q[:4])
+    want = _oracle_search(q, graph, cb, codes, base, t)
+    vec = m in (32, 48)
+    if vec:
+        s.set_adc_variant("auto").set_kernel("auto").search(q[:4])
         assert s.last_stats()["kernel"] == 2  # CTA per query with the smem table (codes fit L2)
-    for variant in variants:
-        res = s.set_adc_variant(variant).search(q)
-        _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
-    if m in (32, 48) and R > 32:
-        os.environ["BANG_PF"] = "1"  # warp 0 prefetches the next row (default when codes exceed L2)
-        try:
-            res = s.set_adc_variant("auto").search(q)
-            assert s.last_stats()["kernel"] == 6
-        finally:
-            del os.environ["BANG_PF"]
-        _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    for variant, kernel in _VARIANTS:
+        if kernel == "cta" and not vec:
+            continue
+        res = s.set_adc_variant(variant).set_kernel(kernel).search(q)
+        _same_as_oracle(res, want)
+    if vec and R > 32:
+        # the prefetching kernel (default when the codes exceed L2)
+        res = s.set_adc_variant("auto").set_kernel("pf").search(q)
+        assert s.last_stats()["kernel"] == 6
+        _same_as_oracle(res, want)
+
+
+# search_pf_kernel data flows: (prefetch warps, staged code rows, early Bloom sets)
+_PF_FLOWS = [(1, 1, 1), (2, 1, 1), (2, 0, 1), (2, 1, 0), (1, 0, 0)]
 
 
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z", [
@@ -366,28 +395,89 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("pf", ["1", "0", "red", "pf2", "red2", "l2", "spec2", "late"])
-def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, pf, monkeypatch):
-    """Default CTA kernel with small Bloom filters: most rows share slots, so
-    the warp replay from pre-state bits (replay_row_warp) runs constantly.
-    pf=1: the prefetching variant (search_pf_kernel, in-row slot sharing
-    from fetch-or results); red: search_pf_kernel with sharing found ahead by
-    warp 0 and fire-and-forget sets; 0: search_cta_kernel."""
-    monkeypatch.setenv("BANG_PF", "0" if pf == "0" else "1")
-    monkeypatch.setenv("BANG_PF_RED", "1" if pf.startswith("red") else "0")
-    monkeypatch.setenv("BANG_PF_WARPS", "2" if pf.endswith("2") else "1")  # 2: two prefetch warps
-    monkeypatch.setenv("BANG_PF_STAGE", "0" if pf == "l2" else "1")  # l2: code rows via L2, not smem
-    monkeypatch.setenv("BANG_PF_SPEC2", "1" if pf == "spec2" else "0")  # two-hop speculative code prefetch
-    monkeypatch.setenv("BANG_PF_EARLY", "0" if pf == "late" else "1")  # late: Bloom sets by the compute threads
+@pytest.mark.parametrize("flow", ["cta", "cta-summary"] + [f"pf{w}{s}{e}" for w, s, e in _PF_FLOWS])
+def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
+    """CTA kernels with small Bloom filters: most rows share slots, so the
+    warp replay from pre-state bits (replay_row_warp) runs constantly.
+    cta: search_cta_kernel (filter cleared per query; -summary: smem bitmap of
+    written words instead); pfWSE: search_pf_kernel with W prefetch warps,
+    staged (S=1) or L2-prefetched code rows, early (E=1) or late Bloom sets."""
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=z, threads=8)
+    if flow.startswith("cta"):
+        s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
+    else:
+        w, st, e = (int(c) for c in flow[2:])
+        s.set_kernel("pf", pf_warps=w, pf_stage=st, pf_early=e)
+    want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
-    assert s.last_stats()["kernel"] == (2 if pf == "0" else 6)
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 6)
+    _same_as_oracle(res, want)
+
+
+# ---- the benchmarked operating point's code paths (VERDICT r1: merge chunks
+# c >= 1 of search_pf_kernel at t > NC and of search_cta_kernel at t > NT)
+# on C3-shaped indexes of 100K nodes (10M x 96 f32 shape, R=64, m=48) and a
+# C2-shaped one (128-d u8, m=32)
+
+_BIG = {}
+
+
+def _big_case(shape):
+    if shape not in _BIG:
+        if shape == "C3":
+            _BIG[shape] = _random_case(21, 100_000, 96, 64, 48, 160, np.float32)
+        else:
+            _BIG[shape] = _random_case(22, 100_000, 128, 64, 32, 160, np.uint8)
+    return _BIG[shape]
+
+
+_ORACLE = {}
+
+
+def _big_oracle(shape, t, z=399_887):
+    key = (shape, t, z)
+    if key not in _ORACLE:
+        base, q, graph, cb, codes = _big_case(shape)
+        _ORACLE[key] = _oracle_search(q, graph, cb, codes, base, t, z)
+    return _ORACLE[key]
+
+
+@pytest.mark.parametrize("t", [100, 166, 256])
+@pytest.mark.parametrize("pfw,stage,early", [(2, 1, 1), (1, 1, 1), (2, 0, 1), (2, 1, 0)])
+def test_pf_kernel_large_t_matches_oracle(t, pfw, stage, early):
+    """search_pf_kernel at worklists spanning 2-4 merge chunks of NC = 64/96
+    threads (t=166 is the C3 benchmark's operating point)."""
+    base, q, graph, cb, codes = _big_case("C3")
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    s.set_kernel("pf", pf_warps=pfw, pf_stage=stage, pf_early=early)
+    res = s.search(q)
+    st = s.last_stats()
+    assert st["kernel"] == 6
+    _same_as_oracle(res, _big_oracle("C3", t))
+
+
+@pytest.mark.parametrize("shape,t", [("C3", 160), ("C3", 300), ("C2", 160), ("C2", 300)])
+def test_cta_kernel_large_t_matches_oracle(shape, t):
+    """search_cta_kernel at worklists spanning 2-3 merge chunks of NT = 128."""
+    base, q, graph, cb, codes = _big_case(shape)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    res = s.set_kernel("cta").search(q)
+    assert s.last_stats()["kernel"] == 2
+    _same_as_oracle(res, _big_oracle(shape, t))
+
+
+def test_pf_kernel_c2_shape_matches_oracle():
+    """search_pf_kernel over 32-byte code rows (m = 32, sub = 4) at t = 200."""
+    base, q, graph, cb, codes = _big_case("C2")
+    s = B.GraphSearcher(k=10, t=200, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    res = s.set_kernel("pf").search(q)
+    assert s.last_stats()["kernel"] == 6
+    _same_as_oracle(res, _big_oracle("C2", 200))
 
 
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
@@ -400,79 +490,32 @@ def test_pipelined_cta_kernel_matches_oracle(seed, n, d, R, m, t, dtype):
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="pipelined", bloom_entries=399_887, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=399_887, threads=8)
+    want = _oracle_search(q, graph, cb, codes, base, t)
     res = s.search(q)
     assert s.last_stats()["kernel"] == 2
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    _same_as_oracle(res, want)
 
 
-@pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank,nq", [
-    (5, 20_000, 96, 64, 48, 32, np.float32, 1021, True, 500),     # collision-heavy Bloom: replay path
-    (6, 20_000, 128, 64, 32, 40, np.uint8, 4099, False, 300),     # no re-rank: wl[0:k] outputs
-    (7, 16_000, 128, 32, 32, 24, np.float32, 399_887, True, 700), # R=32 rows (one probe per thread)
-    (8, 16_000, 96, 48, 48, 100, np.float32, 399_887, True, 5),   # fewer queries than pool slots
-    (9, 16_000, 96, 64, 48, 16, np.float32, 251, True, 400),      # tiny filter: most rows collide
-])
-def test_pool_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank, nq):
-    """search_pool_kernel (lockstep query pool, CTA-shared codebook) against
-    the oracle: visit logs, iterations, ids, dists, short -- bit for bit."""
-    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, nq, dtype)
-    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, rerank=rerank, debug_checks=True)
-    s.fit(base, graph=graph, codebook=cb, codes=codes)
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=z, rerank=rerank, threads=8)
-    res = s.set_adc_variant("pool").search(q)
-    st = s.last_stats()
-    assert st["warps_per_cta"] == 24 and st["adc_variant"] == 0
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
-    assert st["iterations"] == int(res.iterations.sum())
-    if rerank:
-        assert st["rerank_cands"] == int(res.iterations.sum())
-
-
-@pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z,rerank", [
-    (11, 16_000, 96, 64, 48, 40, np.float32, 1021, True),    # collision-heavy: smem replay path
-    (12, 16_000, 128, 64, 32, 32, np.uint8, 251, False),     # tiny filter, no re-rank
-    (13, 16_000, 128, 40, 32, 64, np.float32, 399_887, True),  # R=40: padded slots, uneven degrees
-])
-def test_fat_kernel_matches_oracle(seed, n, d, R, m, t, dtype, z, rerank, monkeypatch):
-    """search_fat_kernel (fat rows, speculative ADC, smem slot-sharing table,
-    fire-and-forget Bloom sets) against the oracle, bit for bit."""
-    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 400, dtype)
-    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, rerank=rerank, debug_checks=True)
-    monkeypatch.setenv("BANG_FAT_ROWS", "1")  # read by bang_index_create
-    s.fit(base, graph=graph, codebook=cb, codes=codes)
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=z, rerank=rerank, threads=8)
-    res = s.search(q)
-    assert s.last_stats()["kernel"] == 3
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
-
-
-def test_pool_kernel_overflow_retry_is_exact():
+@pytest.mark.parametrize("kernel", ["cta", "pf"])
+def test_cta_kernels_overflow_retry_is_exact(kernel):
     from paper_2401_11324_b200 import _lib
     base, q, graph, cb, codes = _random_case(10, 16_000, 96, 64, 48, 200, np.float32)
     t = 64
-    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887).set_adc_variant("pool")
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887).set_kernel(kernel)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     _lib.check(_lib.lib().bang_index_set_log_capacity(s.index_.handle, 60))
     res = s.search(q)
     assert s.last_stats()["retries"] > 0
-    want = O.search(q, centroids=cb.centroids, sub_sizes=cb.subspace_sizes, codes=codes.codes,
-                    adjacency=graph.adjacency, degrees=graph.degrees, medoid=graph.medoid, vectors=base,
-                    k=10, t=t, bloom_entries=399_887, threads=8)
-    _assert_same(res, want["ids"], want["dists"], want["iterations"], want["visit_logs"], want["short"])
+    _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, t))
 
 
-def test_pool_kernel_rejects_unsupported_shapes():
+def test_explicit_kernel_rejects_unsupported_shapes():
     g = gu.load("search_vamana_f32.npz")  # m=4: no 16-byte code rows
-    s = _searcher_from_golden(g).set_adc_variant("pool")
+    s = _searcher_from_golden(g).set_kernel("cta")
     with pytest.raises(B.ParameterError):
         s.search(g["queries"])
+    with pytest.raises(B.ParameterError):
+        s.set_kernel("no-such-kernel")
 
 
 def test_visit_log_overflow_retry_is_exact():
