@@ -34,6 +34,8 @@ typedef int32_t bang_status;
 #define BANG_E_OOM (-3)      /* device allocation failed -> BangError           */
 #define BANG_E_CAPACITY (-4) /* caller buffer too small; sizes reported         */
 #define BANG_E_STATE (-5)    /* handle misuse / debug-check failure             */
+#define BANG_E_FORMAT (-6)   /* malformed index file -> FileFormatError (errors.py:12-13) */
+#define BANG_E_TRUNCATED (-7)/* index file ends early -> TruncatedFileError (errors.py:16-17) */
 
 /* vector scalar kinds (validation.py:8 SUPPORTED_SCALARS) */
 #define BANG_VEC_F32 0
@@ -186,6 +188,18 @@ bang_status bang_search_device(bang_index *index, const float *d_queries, int64_
 /* Synchronises the handle's last device search and reports overflow/debug
  * failures (BANG_E_CAPACITY / BANG_E_STATE), filling the stats. */
 bang_status bang_sync_status(bang_index *index);
+
+/* ------------------------------------------------------------ index load
+ * read_graph (io.py:254-278): the PGIX file ("PGIX", u32 {1, n, R, medoid},
+ * then per node u32 len + len u32 ids) is memory-mapped; one serial pass
+ * walks the length words, then `threads` host threads (0 = all) copy the ids
+ * into the caller's (n, R) int32 adjacency (-1 padded) and degrees (n).
+ * Errors as the reference reader's: BANG_E_FORMAT (bad magic/version, degree
+ * above R, id out of range, trailing bytes), BANG_E_TRUNCATED (short file),
+ * in file order.  Host-only: needs no GPU.                                   */
+bang_status bang_read_graph_header(const char *path, int64_t *n, int32_t *R, int32_t *medoid);
+bang_status bang_read_graph(const char *path, int32_t *adjacency, int32_t *degrees, int64_t n, int32_t R,
+                            int32_t threads);
 
 /* ---------------------------------------------- per-kernel entries (device pointers) */
 

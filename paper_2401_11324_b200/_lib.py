@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import BangError, ParameterError
+from .errors import BangError, FileFormatError, ParameterError, TruncatedFileError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbang.so")
@@ -21,6 +21,8 @@ BANG_E_CUDA = -2
 BANG_E_OOM = -3
 BANG_E_CAPACITY = -4
 BANG_E_STATE = -5
+BANG_E_FORMAT = -6
+BANG_E_TRUNCATED = -7
 
 VEC_F32, VEC_U8, VEC_I8 = 0, 1, 2
 GRAPH_HBM, GRAPH_HOST_MAPPED = 0, 1
@@ -81,6 +83,8 @@ _SIGS = {
     "bang_index_create": (_I32, [_I32, _P, _I64, _I32, _P, _P, _I32, _P, _P, _I32, _I32, _P,
                                  _I32, _I32, ctypes.POINTER(_P)]),
     "bang_index_destroy": (None, [_P]),
+    "bang_read_graph_header": (_I32, [ctypes.c_char_p, _P, _P, _P]),
+    "bang_read_graph": (_I32, [ctypes.c_char_p, _P, _P, _I64, _I32, _I32]),
     "bang_index_info": (_I32, [_P, _P, _P, _P, _P, _P]),
     "bang_index_device_ptrs": (_I32, [_P, _P, _P, _P, _P, _P]),
     "bang_index_code_stride": (_I32, [_P]),
@@ -138,6 +142,10 @@ def check(status: int, what: str = "") -> None:
     msg = last_error() or what
     if status == BANG_E_PARAM:
         raise ParameterError(msg)
+    if status == BANG_E_FORMAT:
+        raise FileFormatError(msg)
+    if status == BANG_E_TRUNCATED:
+        raise TruncatedFileError(msg)
     raise BangError(f"{what}: {msg} (status {status})" if what else msg)
 
 

@@ -38,6 +38,18 @@ bang_status fail(bang_status code, const char *fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+namespace bang {
+// the thread-local message of bang_last_error() for the other translation units
+bang_status set_error_msg(bang_status code, const char *msg) {
+    g_err = msg;
+    return code;
+}
+}  // namespace bang
+
+namespace {
+
 #define CU(call)                                                                         \
     do {                                                                                 \
         cudaError_t e_ = (call);                                                         \

@@ -131,3 +131,39 @@ def test_dataset_generator_matches_reference_stream():
     g = gu.load("search_vamana_f32.npz")
     base, q = gaussian_mixture(3000, 48, 16, clusters=24, seed=101)
     assert np.array_equal(base, g["base"]) and np.array_equal(q, g["queries"])
+
+
+def test_native_graph_reader_matches_reference_cases(tmp_path):
+    """bang_read_graph (native, mmap) against the reference reader's outcome
+    on valid and corrupted PGIX files (tests/golden/make_io_golden.py): the
+    same arrays, or the same exception class and message."""
+    g = gu.load("io_graph_cases.npz")
+    for name in [str(v) for v in g["names"]]:
+        path = tmp_path / f"{name}.pgix"
+        path.write_bytes(g[f"{name}__bytes"].tobytes())
+        if f"{name}__error" in g:
+            cls = getattr(B, str(g[f"{name}__error"]))
+            with pytest.raises(cls) as ei:
+                B.read_graph(str(path))
+            assert type(ei.value).__name__ == str(g[f"{name}__error"]), name
+            assert str(ei.value) == str(g[f"{name}__message"]).replace("{path}", str(path)), name
+        else:
+            got = B.read_graph(str(path))
+            assert np.array_equal(got.adjacency, g[f"{name}__adjacency"]), name
+            assert np.array_equal(got.degrees, g[f"{name}__degrees"]), name
+            assert got.medoid == int(g[f"{name}__medoid"]), name
+
+
+def test_native_graph_reader_threads_agree(tmp_path):
+    """Thread count never changes the result (the copy pass is partitioned by node)."""
+    rng = np.random.default_rng(3)
+    n, R = 20_000, 24
+    deg = rng.integers(0, R + 1, size=n).astype(np.int32)
+    adj = np.full((n, R), -1, np.int32)
+    for i in range(n):
+        ids = rng.choice(n - 1, size=int(deg[i]), replace=False)
+        adj[i, :deg[i]] = ids + (ids >= i)
+    graph = B.GraphIndex(adj, deg, 7, R)
+    B.write_graph(graph, str(tmp_path / "g.pgix"))
+    for threads in (1, 3, 0):
+        assert B.read_graph(str(tmp_path / "g.pgix"), threads=threads) == graph
