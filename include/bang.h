@@ -58,11 +58,14 @@ typedef int32_t bang_status;
  *  the shared codebook, else the HBM table)                                */
 
 /* Search kernels (bang_options.kernel; bang_search_stats.kernel reports the
- * one that ran as 0 search_kernel, 2 search_cta_kernel, 6 search_pf_kernel). */
+ * one that ran as 0 search_kernel, 2 search_cta_kernel, 6 search_pf_kernel,
+ * 8 search_split_kernel). */
 #define BANG_KERNEL_AUTO 0 /* pf when the codes exceed L2 and R > 32, else cta; warp otherwise */
 #define BANG_KERNEL_WARP 1 /* search_kernel: one warp per query, every ADC data flow           */
 #define BANG_KERNEL_CTA 2  /* search_cta_kernel: one CTA per query, per-query smem table       */
 #define BANG_KERNEL_PF 3   /* search_pf_kernel: search_cta_kernel + prefetch warps one hop ahead */
+#define BANG_KERNEL_SPLIT 4 /* search_split_kernel: row warps build the next hop's keys while list
+                              warps merge the previous hop's (HBM graph, t <= 256)               */
 
 /* Per-index tuning (bang_index_set_options); every setting gives identical
  * results -- they only move work between warps and memory levels.
@@ -76,7 +79,8 @@ typedef struct bang_options {
     int32_t bloom_clear; /* 1: search_cta_kernel clears its filter per query; 0: smem
                             summary bitmap of the words this query wrote               */
     int32_t l2_persist;  /* 1: the Bloom filters get an L2-persisting access window      */
-    int32_t profile;     /* with BANG_PROFILE_PHASES: 2 = the prefetch warps' stages     */
+    int32_t profile;     /* with BANG_PROFILE_PHASES: 2 = the prefetch / row warps' stages,
+                            3 = search_split_kernel's list-warp stages                   */
     int32_t reserved[8];
 } bang_options;
 

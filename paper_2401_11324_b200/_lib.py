@@ -36,9 +36,9 @@ CODEBOOK_SMEM = 32
 PROFILE_PHASES = 64
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 # bang_search_stats.kernel -> kernel name
-KERNELS = {0: "search_kernel", 2: "search_cta_kernel", 6: "search_pf_kernel"}
+KERNELS = {0: "search_kernel", 2: "search_cta_kernel", 6: "search_pf_kernel", 8: "search_split_kernel"}
 # bang_options.kernel
-KERNEL_CHOICES = {"auto": 0, "warp": 1, "cta": 2, "pf": 3}
+KERNEL_CHOICES = {"auto": 0, "warp": 1, "cta": 2, "pf": 3, "split": 4}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

@@ -148,7 +148,7 @@ struct bang_index {
 namespace {
 
 // stats.kernel ids (bang.h)
-enum KernelId { kKGeneric = 0, kKCta = 2, kKPf = 6 };
+enum KernelId { kKGeneric = 0, kKCta = 2, kKPf = 6, kKSplit = 8 };
 
 struct Plan {
     int variant = kAdcSmemCodebook;
@@ -192,9 +192,50 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     const int64_t tab_bytes = (int64_t)ix->m * 256 * 4;
     const bool forced_generic = exact || (flags & (BANG_TABLE_GLOBAL | BANG_CODEBOOK_SMEM)) ||
                                 o.kernel == BANG_KERNEL_WARP;
-    if ((o.kernel == BANG_KERNEL_CTA || o.kernel == BANG_KERNEL_PF) && (forced_generic || mv == 0))
+    if ((o.kernel == BANG_KERNEL_CTA || o.kernel == BANG_KERNEL_PF || o.kernel == BANG_KERNEL_SPLIT) &&
+        (forced_generic || mv == 0))
         return fail(BANG_E_PARAM, "the CTA kernels need m = 32 or 48 with the smem table (m=%d, flags=%d)", ix->m,
                     flags);
+    // ---- one CTA per query, row warps + list warps (search_split_kernel)
+    if (!forced_generic && mv > 0 && o.kernel == BANG_KERNEL_SPLIT) {
+        if (ix->row_hdr || t > 256)
+            return fail(BANG_E_PARAM, "search_split_kernel needs an HBM graph and t <= 256 (t=%d)", t);
+        const int spl = rpad <= 64 ? 1 : 2;
+        const int srpad = 64 * spl;
+        pl.variant = kAdcSmemTable;
+        pl.sub = vsub;
+        pl.mv = mv;
+        pl.nt = 128;
+        pl.kernel = kKSplit;
+        int off = 0;
+        auto take = [&](int64_t bytes) { const int o_ = off; off += (int)align_up(bytes, 16); return o_; };
+        pl.off_q = take(4LL * ix->dim);
+        pl.off_wl = take(8LL * t);
+        pl.off_sk = take(8LL * srpad);
+        pl.off_nk = take(8LL * srpad);
+        pl.off_fid = take(2LL * align_up(t, 8) + 2LL * srpad);  // merge ranks (int16)
+        pl.off_code = take(16LL * srpad);  // the row keys, double-buffered
+        // staged code rows (16*MV bytes each); the replay records reuse it
+        pl.off_dup = take(std::max<int64_t>(16LL * mv * srpad, 10LL * srpad));
+        pl.off_alive = take(srpad);        // replay output
+        pl.off_acc = take(256);            // SplitMisc
+        pl.off_vis = take(t);
+        pl.off_tab = take(tab_bytes);
+        pl.per_warp = off;
+        pl.shared_bytes = 0;
+        pl.warps = pl.nt / 32;
+        pl.smem = off;
+        if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
+        pl.fn = pick_split_kernel(spl, pl.sub, pl.mv);
+        if (!pl.fn) return fail(BANG_E_STATE, "no split kernel for pl=%d sub=%d mv=%d", spl, pl.sub, pl.mv);
+        CU(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
+        int per_sm = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.fn, pl.nt, pl.smem));
+        if (per_sm < 1) return fail(BANG_E_CUDA, "search CTA cannot be resident");
+        pl.ctas = (int)std::min<int64_t>((int64_t)ix->sm_count * per_sm, std::max<int64_t>(1, nq));
+        pl.slots = pl.ctas;
+        return BANG_OK;
+    }
     // ---- one CTA per query (search_cta_kernel / search_pf_kernel)
     if (!forced_generic && mv > 0) {
         pl.variant = kAdcSmemTable;
@@ -368,7 +409,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     if (ix->bloom.reserve((size_t)pl.slots * pl.bloom_stride)) return BANG_E_OOM;
     if (ix->rr.reserve((size_t)pl.slots * log_cap)) return BANG_E_OOM;
     const bang_options &o = ix->opts;
-    const bool cta = pl.kernel == kKCta || pl.kernel == kKPf;
+    const bool cta = pl.kernel == kKCta || pl.kernel == kKPf || pl.kernel == kKSplit;
     SearchParams p{};
     p.codes = ix->codes;
     p.code_stride = ix->code_stride;
@@ -411,7 +452,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.adc_variant = pl.variant;
     p.rerank = (flags & BANG_RERANK) ? 1 : 0;
     p.debug = (flags & BANG_DEBUG_CHECKS) ? 1 : 0;
-    p.profile = (flags & BANG_PROFILE_PHASES) ? (o.profile == 2 ? 2 : 1) : 0;
+    p.profile = (flags & BANG_PROFILE_PHASES) ? (o.profile == 2 || o.profile == 3 ? o.profile : 1) : 0;
     p.smem_shared_bytes = pl.shared_bytes;
     p.per_warp_bytes = pl.per_warp;
     p.off_q = pl.off_q;
@@ -941,7 +982,7 @@ void bang_options_default(bang_options *o) {
 
 bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {
     if (!ix || !o) return fail(BANG_E_STATE, "null argument");
-    if (o->kernel < BANG_KERNEL_AUTO || o->kernel > BANG_KERNEL_PF)
+    if (o->kernel < BANG_KERNEL_AUTO || o->kernel > BANG_KERNEL_SPLIT)
         return fail(BANG_E_PARAM, "unknown kernel %d", o->kernel);
     if (o->pf_warps < 0 || o->pf_warps > 2) return fail(BANG_E_PARAM, "pf_warps must be 0, 1 or 2");
     ix->opts = *o;

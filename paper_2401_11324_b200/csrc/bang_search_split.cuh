@@ -1,0 +1,594 @@
+// bang_search_split.cuh -- one CTA per query with the iteration split into two
+// concurrent roles (the paper's one-hop-ahead pipeline, PAPER.md:922-938,
+// carried through the whole memory phase of a hop):
+//
+//   row warps  (warps 0-1, one thread per neighbour slot): for the node just
+//              chosen, load its adjacency row, hash every id into its two
+//              Bloom slots (bloom.py:26-42), read the pre-state bits, perform
+//              the row's sets (fetch-or), gather the code rows straight into
+//              registers and sum their ADC distances from the smem table
+//              (engine.py:99-105); exact in-row slot sharing is replayed
+//              (bloom.py:110-163).  Output: the row's keys in shared memory
+//              and their minimum.
+//   list warps (warps 2-3): meanwhile merge the PREVIOUS row's survivors into
+//              the worklist (kernels.py:44-109, engine.py:210-215), mark and
+//              log the node being expanded (engine.py:167-178) and find the
+//              next unvisited head.
+//
+// They meet once per hop at one CTA barrier.  There the eager winner of the
+// next hop is min(row minimum, head) (engine.py:201-205) and convergence is
+// "no unvisited head and no row key below the truncation threshold"
+// (engine.py:217): the post-merge worklist is all-visited exactly then.  So
+// the critical path of a hop is the row chain alone (row -> {Bloom words,
+// code rows} -> ADC); sort and merge run off it.
+//
+// Semantics are SURVEY.md 8(a0) bit for bit (same as search_cta_kernel).
+#pragma once
+
+#include "bang_search_pf.cuh"  // named barriers, L2 row prefetch, clock_after
+
+namespace bang {
+
+struct SplitMisc {
+    unsigned long long rmin[2][2];  // [parity][row warp]: min key of the row's fresh neighbours
+    unsigned long long head[2];  // [parity]: first unvisited worklist key (SENTINEL if none)
+    unsigned long long thr[2];   // [parity]: wl[t-1] when the worklist is full, else SENTINEL
+    unsigned long long okey;     // list warps: next unvisited old entry after the winner
+    int rfresh[2][2];            // [parity][row warp]: fresh neighbours of the row
+    int rdeg[2];                 // [parity]: degree of the row
+    int hpos[2];                 // [parity]: position of the head
+    int cnt[2];                  // [parity]: worklist entries
+    int wsurv[2];                // list warps: survivors per list warp
+    int opos;                    // list warps: old position of okey (cnt if none)
+    int coll;                    // row warps: in-row slot sharing seen
+    long long qi;
+    unsigned long long ph[8];  // phase profiler
+};
+static_assert(sizeof(SplitMisc) <= 256, "SplitMisc must fit its 256-byte smem slot");
+
+__device__ __forceinline__ void split_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 16 bytes of a code row; read-only for the kernel's lifetime, used once
+__device__ __forceinline__ uint4 ldg_code16(const uint8_t *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t u4_word(const uint4 &v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Row warps: the row of node w -> keys in s_key[0, 64*PL) (SENTINEL for
+// slots past the degree and for neighbours the Bloom filter drops); their
+// minimum and fresh count in s_m (parity `par`).  rt = thread index among
+// the 64 row threads.
+template <int PL, int MV>
+__device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int rt, const float *s_tab,
+                                          uint32_t *bits, uint64_t *s_key, SplitMisc *s_m, int par,
+                                          uint8_t *s_stage, uint8_t *s_tf) {
+    constexpr int M = 16 * MV;
+    constexpr int RPAD = 64 * PL;
+    constexpr int CH = 16;  // table lookups issued ahead of their sums
+    const int rw = rt >> 5, lane = rt & 31;
+    // (p.profile == 2) row thread 0's cycles from entry to each stage, per hop
+    const bool bk = p.profile == 2 && rt == 0;
+    const long long c0 = bk ? clock64() : 0;
+#define SPLIT_STAMP(slot, dep) \
+    if (bk) s_m->ph[slot] += (unsigned long long)(clock_after((int)(dep)) - c0);
+    const int deg = __ldg(p.deg + w);
+    uint32_t nid[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        const int jj = rt + 64 * r;
+        nid[r] = jj < p.R ? (uint32_t)__ldg(p.adj + (int64_t)w * p.adj_stride + jj) : 0u;
+    }
+    SPLIT_STAMP(0, nid[0] ^ (uint32_t)deg)
+    // ---- the Bloom pre-state loads (L2), then the code-row gathers (HBM)
+    // staged into shared memory by cp.async: their completion is tracked
+    // apart from the Bloom words', so the Bloom test and the row's sets do
+    // not wait for HBM
+    uint32_t p1[PL], p2[PL], wd1[PL], wd2[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
+        if (rt + 64 * r < deg) {
+            p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
+            p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
+            wd1[r] = __ldcg(bits + (p1[r] >> 5));
+            wd2[r] = __ldcg(bits + (p2[r] >> 5));
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        if (rt + 64 * r < deg) {
+            const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
+#pragma unroll
+            for (int v = 0; v < MV; ++v)
+                __pipeline_memcpy_async(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v, 16);
+        }
+    }
+    __pipeline_commit();
+    // ---- Bloom test against the pre-state (bloom.py:70-75 semantics)
+    bool pf[PL], b1[PL], b2[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        b1[r] = (wd1[r] >> (p1[r] & 31)) & 1u;
+        b2[r] = (wd2[r] >> (p2[r] & 31)) & 1u;
+        pf[r] = rt + 64 * r < deg && !(b1[r] && b2[r]);
+    }
+    SPLIT_STAMP(1, pf[0])
+    if (rt == 0) s_m->coll = 0;
+    // every row thread holds its pre-state words before any set of this row
+    // lands (the words are consumed above)
+    split_bar(3, 64);
+    SPLIT_STAMP(2, 0)
+    uint32_t o1[PL], o2[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        o1[r] = o2[r] = 0u;
+        if (pf[r]) {
+            o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
+            if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
+        }
+    }
+    // ---- ADC of the presumed-fresh neighbours while the fetch-ors return:
+    // acc = ((0 + T[0][c0]) + T[1][c1]) + ... in f32 (engine.py:99-105); the
+    // lookups of a chunk are issued before its sums
+    __pipeline_wait_prior(0);  // this thread's own staged rows
+    float acc[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        acc[r] = 0.0f;
+        if (pf[r]) {
+            uint4 code[MV];
+#pragma unroll
+            for (int v = 0; v < MV; ++v)
+                code[v] = *reinterpret_cast<const uint4 *>(s_stage + (rt + 64 * r) * M + 16 * v);
+#pragma unroll
+            for (int s0 = 0; s0 < M; s0 += CH) {
+                float e[CH];
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int s = s0 + q;
+                    const uint32_t word = u4_word(code[s >> 4], (s >> 2) & 3);
+                    e[q] = s_tab[s * 256 + ((word >> (8 * (s & 3))) & 0xFFu)];
+                }
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[r] = __fadd_rn(acc[r], e[q]);
+            }
+        }
+    }
+    SPLIT_STAMP(3, __float_as_int(acc[0]))
+    // ---- in-row slot sharing: a fetch-or found its bit set although the
+    // pre-state lacked it -> another probe of this row set it first
+    bool sh1[PL], sh2[PL];
+    bool any_sh = false;
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        sh1[r] = pf[r] && !b1[r] && ((o1[r] >> (p1[r] & 31)) & 1u);
+        sh2[r] = pf[r] && p2[r] != p1[r] && !b2[r] && ((o2[r] >> (p2[r] & 31)) & 1u);
+        any_sh = any_sh || sh1[r] || sh2[r];
+    }
+    SPLIT_STAMP(4, any_sh)
+    if (any_sh) s_m->coll = 1;
+    split_bar(3, 64);
+    SPLIT_STAMP(5, 0)
+    bool fresh[PL];
+#pragma unroll
+    for (int r = 0; r < PL; ++r) fresh[r] = pf[r];
+    if (s_m->coll) {
+        // rare (~2% of rows at z = 399,887): exact sequential replay of the
+        // involved probes by row warp 0 from the pre-state bits; the records
+        // go where the (consumed) code rows were staged
+        uint2 *s_rec = reinterpret_cast<uint2 *>(s_stage);
+        uint8_t *s_fl2 = s_stage + 8 * RPAD;
+        split_bar(3, 64);  // every row thread has read its staged rows
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            const int jj = rt + 64 * r;
+            s_rec[jj] = make_uint2(p1[r], p2[r]);
+            s_fl2[2 * jj] = (uint8_t)((pf[r] ? 2 : 0) | (b1[r] ? 4 : 0) | (sh1[r] ? 8 : 0));
+            s_fl2[2 * jj + 1] = (uint8_t)((b2[r] ? 4 : 0) | (sh2[r] ? 8 : 0));
+        }
+        split_bar(3, 64);
+        if (rw == 0) replay_row_warp<RPAD / 32>(s_rec, s_fl2, deg, bits, s_tf);
+        split_bar(3, 64);
+#pragma unroll
+        for (int r = 0; r < PL; ++r) fresh[r] = rt + 64 * r < deg && s_tf[rt + 64 * r];
+    }
+    // keys out; per-warp minimum (dist bits, then id: two 32-bit
+    // reductions) and fresh count
+    int fc = 0;
+    uint64_t mn = kSentinel;
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        const uint64_t key = fresh[r] ? pack_key(acc[r], nid[r]) : kSentinel;
+        s_key[rt + 64 * r] = key;
+        mn = key < mn ? key : mn;
+        fc += fresh[r];
+    }
+    const uint32_t mhi = __reduce_min_sync(kFull, (uint32_t)(mn >> 32));
+    const uint32_t mlo = __reduce_min_sync(kFull, (uint32_t)(mn >> 32) == mhi ? (uint32_t)mn : 0xFFFFFFFFu);
+    fc = __reduce_add_sync(kFull, fc);
+    if (lane == 0) {
+        s_m->rmin[par][rw] = ((uint64_t)mhi << 32) | mlo;
+        s_m->rfresh[par][rw] = fc;
+    }
+    if (rt == 0) s_m->rdeg[par] = deg;
+    SPLIT_STAMP(6, fc)
+#undef SPLIT_STAMP
+}
+
+// List warps: merge the survivors of s_key (keys < thr) into the worklist
+// (kernels.py:68-87: rank of each entry in the other list, old entries first
+// on ties -- keys are unique), mark the winner visited and log it, publish
+// the next head / threshold / count at parity `nxt`.  lt = thread index
+// among the 64 list threads.  s_c (t int16): survivors below each old entry;
+// s_spos (RPAD int16): final position of each sorted survivor.
+template <int PL>
+__device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64_t *s_wl, uint8_t *s_vis,
+                                           const uint64_t *s_key, uint64_t *s_nk, uint64_t *s_sk, int16_t *s_c,
+                                           int16_t *s_spos, SplitMisc *s_m, int nxt, uint64_t winner,
+                                           uint64_t head, uint64_t thr, int cnt, int hpos, int32_t *log, int iters) {
+    constexpr int NC = 64;      // list threads
+    constexpr int MAXCH = 4;    // worklists up to 4*NC entries (checked on the host)
+    constexpr int H = 32 * PL;  // survivors region per list warp
+    const int lane = lt & 31, lw = lt >> 5;
+    const int t = p.t;
+    const unsigned ltm = (1u << lane) - 1u;
+    const bool won_head = winner == head;
+    // (p.profile == 3) list thread 0's cycles from entry to each stage, per hop
+    const bool bk = p.profile == 3 && lt == 0;
+    const long long c0 = bk ? clock64() : 0;
+#define SPLIT_STAMP(slot, dep) \
+    if (bk) s_m->ph[slot] += (unsigned long long)(clock_after((int)(dep)) - c0);
+    // ---- survivors (keys < thr: ranks >= t are truncated, engine.py:213)
+    // compacted per list warp in adjacency order
+    uint64_t k[PL];
+    bool sv[PL];
+    int cw = 0;
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        k[r] = s_key[lt + 64 * r];
+        sv[r] = k[r] < thr;
+        const unsigned b = __ballot_sync(kFull, sv[r]);
+        if (sv[r]) s_nk[H * lw + cw + __popc(b & ltm)] = k[r];
+        cw += __popc(b);
+    }
+    if (lane == 0) s_m->wsurv[lw] = cw;
+    // the next unvisited old entry after the winner: the old head itself, or
+    // (the head won) the first unvisited entry after it
+    if (lw == 0) {
+        const int op = won_head ? first_unvisited(s_vis, hpos + 1, cnt) : hpos;
+        if (lane == 0) {
+            s_m->opos = op;
+            s_m->okey = op < cnt ? s_wl[op] : kSentinel;
+        }
+    }
+    split_bar(4, NC);
+    const int c0w = s_m->wsurv[0], c1w = s_m->wsurv[1];
+    const int n = c0w + c1w;
+    SPLIT_STAMP(0, n)
+    // ---- kernel 4a: rank sort of the survivors (broadcast reads)
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        if (sv[r]) {
+            int rk = 0;
+            for (int i = 0; i < c0w; ++i) rk += s_nk[i] < k[r];
+            for (int i = 0; i < c1w; ++i) rk += s_nk[H + i] < k[r];
+            s_sk[rk] = k[r];
+        }
+    }
+    split_bar(4, NC);
+    SPLIT_STAMP(1, 0)
+    // ---- kernel 4b: each old entry's count of smaller survivors (the
+    // chunks' binary searches interleaved step by step)
+    const int nch = (cnt + NC - 1) / NC;
+    uint64_t mv[MAXCH];
+    uint8_t mvv[MAXCH];
+    int mc[MAXCH];
+#pragma unroll
+    for (int c = 0; c < MAXCH; ++c) {
+        const int i = c * NC + lt;
+        mv[c] = kSentinel;
+        mvv[c] = 0;
+        mc[c] = 0;
+        if (c < nch && i < cnt) {
+            mv[c] = s_wl[i];
+            mvv[c] = s_vis[i];
+        }
+    }
+    if (n > 0) {
+        for (int step = 1 << (31 - __clz(n)); step > 0; step >>= 1) {
+#pragma unroll
+            for (int c = 0; c < MAXCH; ++c)
+                if (c < nch && mc[c] + step <= n && s_sk[mc[c] + step - 1] < mv[c]) mc[c] += step;
+        }
+#pragma unroll
+        for (int c = 0; c < MAXCH; ++c)
+            if (c < nch && c * NC + lt < cnt) s_c[c * NC + lt] = (int16_t)mc[c];
+    }
+    SPLIT_STAMP(2, mc[0])
+    split_bar(4, NC);  // all reads of the old worklist precede the writes
+    // ---- merge + truncate to t (engine.py:210-215): old entry i goes to
+    // i + c_i; survivors c_{i-1} .. c_i - 1 land just before it, the rest
+    // after the last old entry
+    if (n > 0) {
+#pragma unroll
+        for (int c = 0; c < MAXCH; ++c) {
+            const int i = c * NC + lt;
+            if (c < nch && i < cnt) {
+                const int ci = mc[c];
+                const int prev = i > 0 ? s_c[i - 1] : 0;
+                if (i + ci < t) {
+                    s_wl[i + ci] = mv[c];
+                    s_vis[i + ci] = mvv[c];
+                }
+                for (int r = prev; r < ci; ++r) {
+                    s_spos[r] = (int16_t)(i + r);
+                    if (i + r < t) {
+                        s_wl[i + r] = s_sk[r];
+                        s_vis[i + r] = 0;
+                    }
+                }
+                if (i == cnt - 1)
+                    for (int r = ci; r < n; ++r) {
+                        s_spos[r] = (int16_t)(cnt + r);
+                        if (cnt + r < t) {
+                            s_wl[cnt + r] = s_sk[r];
+                            s_vis[cnt + r] = 0;
+                        }
+                    }
+            }
+        }
+    }
+    const int ncnt = min(t, cnt + n);
+    split_bar(4, NC);  // the merged worklist is complete
+    SPLIT_STAMP(3, 0)
+    // ---- expand the winner (engine.py:167-178); the next head is the
+    // smaller of the next old unvisited entry and the best survivor other
+    // than the winner, at its merged position (none if truncated)
+    if (lt == 0) {
+        // loads first (the stores below may alias them for the compiler)
+        const int op = s_m->opos;
+        uint64_t hk = s_m->okey;
+        const int rs = won_head ? 0 : 1;  // best survivor other than the winner
+        const int c_h = n > 0 && won_head ? s_c[hpos] : 0;
+        const int c_o = n > 0 && op < cnt ? s_c[op] : 0;
+        const int sp0 = n > 0 ? s_spos[0] : 0;
+        const uint64_t skr = rs < n ? s_sk[rs] : kSentinel;
+        const int spr = rs < n ? s_spos[rs] : t;
+        const uint64_t last = s_wl[t - 1];
+        const int wpos = won_head ? hpos + c_h : sp0;
+        if (p.debug && (wpos >= t || s_wl[wpos] != winner)) atomicAdd(p.counters + kCtrDebugFail, 1ull);
+        int hp = op < cnt ? op + c_o : t;
+        if (skr < hk) {
+            hk = skr;
+            hp = spr;
+        }
+        if (hp >= ncnt) {
+            hk = kSentinel;
+            hp = ncnt;
+        }
+        if (wpos < t) s_vis[wpos] = 1;
+        if (iters < p.log_cap) log[iters] = (int32_t)key_id(winner);
+        s_m->hpos[nxt] = hp;
+        s_m->head[nxt] = hk;
+        s_m->thr[nxt] = ncnt == t ? last : kSentinel;
+        s_m->cnt[nxt] = ncnt;
+        // the head may be the next winner: its row to L2
+        if (p.pf_spec && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
+    }
+    SPLIT_STAMP(4, 0)
+#undef SPLIT_STAMP
+}
+
+template <int PL, int SUB, int MV>
+__global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(const SearchParams p) {
+    constexpr int NT = 128;
+    constexpr int M = 16 * MV;
+    constexpr int RPAD = 64 * PL;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    const bool roww = tid < 64;  // row warps 0-1, list warps 2-3
+
+    float *s_q = reinterpret_cast<float *>(smem + p.off_q);
+    uint64_t *s_wl = reinterpret_cast<uint64_t *>(smem + p.off_wl);
+    uint64_t *s_sk = reinterpret_cast<uint64_t *>(smem + p.off_sk);
+    uint64_t *s_nk = reinterpret_cast<uint64_t *>(smem + p.off_nk);
+    uint64_t *s_key = reinterpret_cast<uint64_t *>(smem + p.off_code);  // [2][RPAD]
+    int16_t *s_c = reinterpret_cast<int16_t *>(smem + p.off_fid);          // [t]
+    int16_t *s_spos = s_c + ((p.t + 7) & ~7);                              // [RPAD]
+    uint8_t *s_stage = smem + p.off_dup;  // [RPAD][M] staged code rows / replay records
+    uint8_t *s_tf = smem + p.off_alive;                                   // [RPAD]
+    uint8_t *s_vis = smem + p.off_vis;
+    float *s_tab = reinterpret_cast<float *>(smem + p.off_tab);
+    SplitMisc *s_m = reinterpret_cast<SplitMisc *>(smem + p.off_acc);
+    uint32_t *bits = p.bloom + (int64_t)blockIdx.x * p.bloom_stride;
+    uint64_t *rr = p.rr_scratch + (int64_t)blockIdx.x * p.log_cap;
+    const int t = p.t;
+
+    unsigned long long st_iters = 0, st_probes = 0, st_fresh = 0, st_rr = 0;
+    // phase profiler (p.profile): 0 row chain (row thread 0), 1 list step
+    // (list thread 0), 2/3 their waits at the hop barrier, 7 per-query prologue
+    // + epilogue (thread 0)
+    if (tid == 0)
+        for (int i = 0; i < 8; ++i) s_m->ph[i] = 0;
+    const bool prof = p.profile == 1 && (tid == 0 || tid == 64);
+
+    for (;;) {
+        long long c_q = p.profile ? clock64() : 0;
+        if (tid == 0) s_m->qi = (long long)atomicAdd(p.counters + kCtrNextQuery, 1ull);
+        __syncthreads();
+        const int64_t qi = s_m->qi;
+        if (qi >= p.nq) break;
+        const int64_t qid = p.query_map ? (int64_t)p.query_map[qi] : qi;
+
+        for (int i = tid; i < p.dim; i += NT) s_q[i] = __ldg(p.queries + qid * p.dim + i);
+        for (int i = tid; i < t; i += NT) s_vis[i] = 0;
+        {   // the filter starts empty (whole-line stores)
+            uint4 *b4 = reinterpret_cast<uint4 *>(bits);
+            const int n4 = (int)(p.bloom_stride >> 2);
+            for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
+        }
+        __syncthreads();
+        // kernel 1 for this query into shared memory (pq.py:284-296)
+        for (int idx = tid; idx < M * 256; idx += NT) {
+            const int s = idx >> 8, c = idx & 255;
+            float e;
+            if constexpr (SUB == 4) {
+                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                                 __ldg(reinterpret_cast<const float4 *>(p.centroids) + s * 256 + c));
+            } else if constexpr (SUB == 2) {
+                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                                 __ldg(reinterpret_cast<const float2 *>(p.centroids) + s * 256 + c));
+            } else {
+                const int off = __ldg(p.sub_off + s), sz = __ldg(p.sub_size + s);
+                const float *src = p.centroids + (int64_t)off * 256 + c * sz;
+                float dd = __fsub_rn(s_q[off], __ldg(src));
+                float a = __fmul_rn(dd, dd);
+                for (int q = 1; q < sz; ++q) {
+                    dd = __fsub_rn(s_q[off + q], __ldg(src + q));
+                    a = __fadd_rn(a, __fmul_rn(dd, dd));
+                }
+                e = a;
+            }
+            s_tab[idx] = e;
+        }
+        if (tid == 0) {  // the medoid in the filter (engine.py:127-128)
+            const uint32_t w1 = p.medoid_p1 >> 5, w2 = p.medoid_p2 >> 5;
+            const uint32_t b1 = 1u << (p.medoid_p1 & 31), b2 = 1u << (p.medoid_p2 & 31);
+            if (w1 == w2) {
+                __stcg(bits + w1, b1 | b2);
+            } else {
+                __stcg(bits + w1, b1);
+                __stcg(bits + w2, b2);
+            }
+        }
+        __syncthreads();
+        int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
+        if (tid == 64) {
+            // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125), expanded at once
+            const uint8_t *row = p.codes + (int64_t)p.medoid * p.code_stride;
+            float acc = 0.0f;
+            for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
+            s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
+            s_vis[0] = 1;
+            if (p.log_cap > 0) log[0] = p.medoid;
+            s_m->head[0] = kSentinel;
+            s_m->hpos[0] = 1;
+            s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
+            s_m->cnt[0] = 1;
+        }
+        if (roww) split_row<PL, MV>(p, (uint32_t)p.medoid, tid, s_tab, bits, s_key, s_m, 0, s_stage, s_tf);
+        if (p.profile && tid == 0) {
+            const long long now_ = clock64();
+            s_m->ph[7] += (unsigned long long)(now_ - c_q);
+        }
+        __syncthreads();
+
+        int iters = 1, par = 0;
+        for (;;) {
+            // ---- the hop barrier: eager winner and convergence (engine.py:201-217)
+            const uint64_t rmin = min(s_m->rmin[par][0], s_m->rmin[par][1]);
+            const uint64_t head = s_m->head[par];
+            const uint64_t thr = s_m->thr[par];
+            const uint64_t winner = rmin < head ? rmin : head;
+            st_probes += s_m->rdeg[par];
+            st_fresh += s_m->rfresh[par][0] + s_m->rfresh[par][1];
+            if (head == kSentinel && !(rmin < thr)) break;  // merged worklist all visited
+            const long long c0 = prof ? clock64() : 0;
+            if (roww) {
+                split_row<PL, MV>(p, key_id(winner), tid, s_tab, bits, s_key + (par ^ 1) * RPAD, s_m, par ^ 1,
+                                  s_stage, s_tf);
+            } else {
+                split_list<PL>(p, tid - 64, s_wl, s_vis, s_key + par * RPAD, s_nk, s_sk, s_c, s_spos, s_m, par ^ 1,
+                               winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters);
+            }
+            long long c1 = 0;
+            if (prof) {
+                c1 = clock64();
+                s_m->ph[tid == 0 ? 0 : 1] += (unsigned long long)(c1 - c0);
+            }
+            ++iters;
+            par ^= 1;
+            __syncthreads();
+            if (prof) s_m->ph[tid == 0 ? 2 : 3] += (unsigned long long)(clock_after(s_m->cnt[par]) - c1);
+        }
+        st_iters += iters;
+        c_q = p.profile ? clock64() : 0;
+
+        // ---- outputs (engine.py:244-269)
+        const int cnt = s_m->cnt[par];
+        int32_t *oid = p.out_ids + qid * p.k;
+        float *odist = p.out_dists + qid * p.k;
+        if (tid == 0) {
+            p.out_iters[qid] = iters;
+            p.out_wall_ns[qid] = globaltimer_ns() - p.counters[kCtrT0];
+        }
+        if (p.rerank) {
+            if (iters > p.log_cap) {  // visit log truncated: the host re-runs this query
+                if (tid == 0) {
+                    const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+                    p.overflow_list[at] = (int32_t)qid;
+                }
+                __syncthreads();
+                continue;
+            }
+            // kernel 5: exact distances of the visit log, then top-k (warp 0)
+            __threadfence_block();
+            __syncthreads();
+            const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
+            if (rowb % 16 == 0 && rowb <= M * 256 * 4) {
+                // the table is dead until the next query: stage rows in its place
+                rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), M * 256 * 4, rr);
+            } else {
+                for (int i = tid; i < iters; i += NT) {
+                    const uint32_t node = (uint32_t)__ldcg(log + i);
+                    rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+                }
+            }
+            st_rr += (tid == 0) ? iters : 0;
+            __threadfence_block();
+            __syncthreads();
+            if (tid < 32) {
+                warp_topk_write(rr, iters, p.k, oid, odist);
+                if (tid == 0) p.out_short[qid] = iters < p.k;
+            }
+        } else {
+            if (p.log_cap < iters && tid == 0) {
+                const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+                p.overflow_list[at] = (int32_t)qid;
+            }
+            for (int q = tid; q < p.k; q += NT) {
+                if (q < cnt) {
+                    oid[q] = (int32_t)key_id(s_wl[q]);
+                    odist[q] = key_dist(s_wl[q]);
+                } else {
+                    oid[q] = -1;
+                    odist[q] = __int_as_float(0x7f800000);
+                }
+            }
+            if (tid == 0) p.out_short[qid] = cnt < p.k;
+        }
+        __syncthreads();
+        if (p.profile && tid == 0) s_m->ph[7] += (unsigned long long)(clock64() - c_q);
+    }
+    if (p.profile && tid == 0) {
+        __syncwarp();
+        // slots written by row thread 0 / list thread 0 of this CTA; all
+        // writers are past the CTA's last barrier
+#pragma unroll
+        for (int i = 0; i < 8; ++i) atomicAdd(p.counters + kCtrPhase0 + i, s_m->ph[i]);
+    }
+    if (tid == 0) {
+        atomicAdd(p.counters + kCtrIterations, st_iters);
+        atomicAdd(p.counters + kCtrRerank, st_rr);
+        atomicAdd(p.counters + kCtrProbes, st_probes);
+        atomicAdd(p.counters + kCtrFresh, st_fresh);
+    }
+}
+
+}  // namespace bang

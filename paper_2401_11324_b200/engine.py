@@ -369,7 +369,7 @@ class GraphSearcher(BaseEstimator):
         return self
 
     def set_kernel(self, kernel: str = "auto", **tuning) -> "GraphSearcher":
-        """Pick the search kernel ("auto", "warp", "cta", "pf") and its tuning
+        """Pick the search kernel ("auto", "warp", "cta", "pf", "split") and its tuning
         (bang_options in include/bang.h).  Results are identical for every
         choice; this only moves work between warps and memory levels."""
         self._kernel_options = dict(kernel=kernel, **tuning)

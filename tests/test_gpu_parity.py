@@ -384,6 +384,10 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
         res = s.set_adc_variant("auto").set_kernel("pf").search(q)
         assert s.last_stats()["kernel"] == 6
         _same_as_oracle(res, want)
+    if vec:
+        res = s.set_adc_variant("auto").set_kernel("split").search(q)
+        assert s.last_stats()["kernel"] == 8
+        _same_as_oracle(res, want)
 
 
 # search_pf_kernel data flows: (prefetch warps, staged code rows, early Bloom sets)
@@ -395,7 +399,7 @@ _PF_FLOWS = [(1, 1, 1), (2, 1, 1), (2, 0, 1), (2, 1, 0), (1, 0, 0)]
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("flow", ["cta", "cta-summary"] + [f"pf{w}{s}{e}" for w, s, e in _PF_FLOWS])
+@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split"] + [f"pf{w}{s}{e}" for w, s, e in _PF_FLOWS])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
     """CTA kernels with small Bloom filters: most rows share slots, so the
     warp replay from pre-state bits (replay_row_warp) runs constantly.
@@ -407,12 +411,14 @@ def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, f
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     if flow.startswith("cta"):
         s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
+    elif flow == "split":
+        s.set_kernel("split")
     else:
         w, st, e = (int(c) for c in flow[2:])
         s.set_kernel("pf", pf_warps=w, pf_stage=st, pf_early=e)
     want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
-    assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 6)
+    assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8 if flow == "split" else 6)
     _same_as_oracle(res, want)
 
 
@@ -459,6 +465,57 @@ def test_pf_kernel_large_t_matches_oracle(t, pfw, stage, early):
     _same_as_oracle(res, _big_oracle("C3", t))
 
 
+@pytest.mark.parametrize("shape,t", [("C3", 100), ("C3", 166), ("C3", 256), ("C2", 80), ("C2", 200)])
+def test_split_kernel_large_t_matches_oracle(shape, t):
+    """search_split_kernel at worklists spanning 2-4 merge chunks of its 64
+    list threads (t=166 is the C3 benchmark's operating point)."""
+    base, q, graph, cb, codes = _big_case(shape)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    res = s.set_kernel("split").search(q)
+    assert s.last_stats()["kernel"] == 8
+    _same_as_oracle(res, _big_oracle(shape, t))
+
+
+@pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
+    (23, 16_000, 96, 100, 48, 120, np.float32),  # 64 < R <= 128: two slots per row thread
+    (24, 16_000, 128, 128, 32, 200, np.uint8),
+    (25, 16_000, 96, 40, 48, 30, np.float32),    # R < 64: idle row threads
+])
+def test_wide_and_narrow_rows_match_oracle(seed, n, d, R, m, t, dtype):
+    base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 200, dtype)
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = _oracle_search(q, graph, cb, codes, base, t)
+    for kernel, kid in (("split", 8), ("cta", 2)):
+        res = s.set_kernel(kernel).search(q)
+        assert s.last_stats()["kernel"] == kid
+        _same_as_oracle(res, want)
+
+
+@pytest.mark.parametrize("t,k", [(1, 1), (10, 10), (11, 10)])
+@pytest.mark.parametrize("kernel", ["split", "cta", "pf"])
+def test_cta_kernels_tiny_worklists_match_oracle(t, k, kernel):
+    """t = k down to 1: the threshold is the single entry, heads run out at once."""
+    base, q, graph, cb, codes = _random_case(26, 8_000, 96, 64, 48, 100, np.float32)
+    s = B.GraphSearcher(k=k, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    for rerank in (True, False):
+        s.rerank = rerank
+        res = s.set_kernel(kernel).search(q)
+        _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, t, rerank=rerank, k=k))
+
+
+@pytest.mark.parametrize("kernel", ["split", "pf", "cta"])
+def test_cta_kernels_without_rerank_match_oracle(kernel):
+    """rerank=False: the outputs are the final worklist's first k entries."""
+    base, q, graph, cb, codes = _big_case("C3")
+    s = B.GraphSearcher(k=10, t=120, mode="in_memory", bloom_entries=399_887, rerank=False, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    res = s.set_kernel(kernel).search(q)
+    _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, 120, rerank=False))
+
+
 @pytest.mark.parametrize("shape,t", [("C3", 160), ("C3", 300), ("C2", 160), ("C2", 300)])
 def test_cta_kernel_large_t_matches_oracle(shape, t):
     """search_cta_kernel at worklists spanning 2-3 merge chunks of NT = 128."""
@@ -496,7 +553,7 @@ def test_pipelined_cta_kernel_matches_oracle(seed, n, d, R, m, t, dtype):
     _same_as_oracle(res, want)
 
 
-@pytest.mark.parametrize("kernel", ["cta", "pf"])
+@pytest.mark.parametrize("kernel", ["cta", "pf", "split"])
 def test_cta_kernels_overflow_retry_is_exact(kernel):
     from paper_2401_11324_b200 import _lib
     base, q, graph, cb, codes = _random_case(10, 16_000, 96, 64, 48, 200, np.float32)
