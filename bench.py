@@ -278,8 +278,8 @@ def main():
     ap.add_argument("--profile", action="store_true", help="1 warm step + 1 step for ncu; no baselines")
     ap.add_argument("--phases", action="store_true", help="per-phase cycle profile (diagnostic)")
     ap.add_argument("--variant", default="auto", choices=("auto", "smem-table", "codebook", "hbm-table"))
-    ap.add_argument("--kernel", default="auto", choices=("auto", "warp", "cta", "pf", "split"))
-    ap.add_argument("--opt", action="append", default=[], help="bang_options field=value (e.g. pf_warps=1)")
+    ap.add_argument("--kernel", default="auto", choices=("auto", "warp", "cta", "split"))
+    ap.add_argument("--opt", action="append", default=[], help="bang_options field=value (e.g. row_prefetch=0)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -574,12 +574,7 @@ def main():
     if args.phases:
         pc = s_last["phase_cycles"]
         it = max(1, s_last["iterations"])
-        if s_last.get("kernel") == 6:  # search_pf_kernel: thread 32's cycles, slot 1 = warp 0's prefetch
-            names = ["bloom_test", "prefetch_warp0", "adc_reduce", "coll_sync", "survivors_sync", "sort",
-                     "merge_and_final_sync"]
-            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
-            out["phase_cycles_per_iteration"]["prologue_epilogue_per_query"] = round(pc[7] / max(1, nq), 1)
-        elif s_last.get("kernel") == 8:  # search_split_kernel: row thread 0 / list thread 0 per hop
+        if s_last.get("kernel") == 8:  # search_split_kernel: row thread 0 / list thread 0 per hop
             prof = searcher.index_.options().get("profile", 0)
             names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "fetch_or_back", "coll_bar", "row_end"],
                      3: ["compact", "sort", "merge_reads", "merge_writes", "list_end"]}.get(

@@ -58,30 +58,25 @@ typedef int32_t bang_status;
  *  the shared codebook, else the HBM table)                                */
 
 /* Search kernels (bang_options.kernel; bang_search_stats.kernel reports the
- * one that ran as 0 search_kernel, 2 search_cta_kernel, 6 search_pf_kernel,
- * 8 search_split_kernel). */
-#define BANG_KERNEL_AUTO 0 /* pf when the codes exceed L2 and R > 32, else cta; warp otherwise */
-#define BANG_KERNEL_WARP 1 /* search_kernel: one warp per query, every ADC data flow           */
-#define BANG_KERNEL_CTA 2  /* search_cta_kernel: one CTA per query, per-query smem table       */
-#define BANG_KERNEL_PF 3   /* search_pf_kernel: search_cta_kernel + prefetch warps one hop ahead */
+ * one that ran as 0 search_kernel, 2 search_cta_kernel, 8 search_split_kernel). */
+#define BANG_KERNEL_AUTO 0  /* split for an HBM graph and t <= 256 (m = 32/48), else cta; warp otherwise */
+#define BANG_KERNEL_WARP 1  /* search_kernel: one warp per query, every ADC data flow               */
+#define BANG_KERNEL_CTA 2   /* search_cta_kernel: one CTA per query, per-query smem table          */
 #define BANG_KERNEL_SPLIT 4 /* search_split_kernel: row warps build the next hop's keys while list
-                              warps merge the previous hop's (HBM graph, t <= 256)               */
+                               warps merge the previous hop's (HBM graph, t <= 256)               */
 
 /* Per-index tuning (bang_index_set_options); every setting gives identical
  * results -- they only move work between warps and memory levels.
  * bang_options_default() fills the measured-best defaults.               */
 typedef struct bang_options {
-    int32_t kernel;      /* BANG_KERNEL_*                                               */
-    int32_t pf_warps;    /* search_pf_kernel prefetch warps: 0 auto, 1 or 2             */
-    int32_t pf_stage;    /* 1: next row's code rows staged in smem when they fit; 0: L2 */
-    int32_t pf_early;    /* 1: the prefetch warps perform the next row's Bloom sets     */
-    int32_t pf_spec;     /* 1: L2 prefetch of the candidate winners' adjacency rows     */
-    int32_t bloom_clear; /* 1: search_cta_kernel clears its filter per query; 0: smem
-                            summary bitmap of the words this query wrote               */
-    int32_t l2_persist;  /* 1: the Bloom filters get an L2-persisting access window      */
-    int32_t profile;     /* with BANG_PROFILE_PHASES: 2 = the prefetch / row warps' stages,
-                            3 = search_split_kernel's list-warp stages                   */
-    int32_t reserved[8];
+    int32_t kernel;       /* BANG_KERNEL_*                                               */
+    int32_t row_prefetch; /* 1: L2 prefetch of the next head's adjacency row (split)      */
+    int32_t bloom_clear;  /* 1: search_cta_kernel clears its filter per query; 0: smem
+                             summary bitmap of the words this query wrote               */
+    int32_t l2_persist;   /* 1: the Bloom filters get an L2-persisting access window      */
+    int32_t profile;      /* with BANG_PROFILE_PHASES: 2 = search_split_kernel's row-warp
+                             stages, 3 = its list-warp stages                            */
+    int32_t reserved[11];
 } bang_options;
 
 typedef struct bang_index bang_index;

@@ -36,9 +36,9 @@ CODEBOOK_SMEM = 32
 PROFILE_PHASES = 64
 ADC_VARIANTS = {0: "smem-codebook", 1: "hbm-table", 2: "exact", 3: "smem-table"}
 # bang_search_stats.kernel -> kernel name
-KERNELS = {0: "search_kernel", 2: "search_cta_kernel", 6: "search_pf_kernel", 8: "search_split_kernel"}
+KERNELS = {0: "search_kernel", 2: "search_cta_kernel", 8: "search_split_kernel"}
 # bang_options.kernel
-KERNEL_CHOICES = {"auto": 0, "warp": 1, "cta": 2, "pf": 3, "split": 4}
+KERNEL_CHOICES = {"auto": 0, "warp": 1, "cta": 2, "split": 4}
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -48,9 +48,8 @@ _I32 = ctypes.c_int32
 class Options(ctypes.Structure):
     """bang_options (include/bang.h): per-index kernel choice and tuning."""
     _fields_ = [
-        ("kernel", ctypes.c_int32), ("pf_warps", ctypes.c_int32), ("pf_stage", ctypes.c_int32),
-        ("pf_early", ctypes.c_int32), ("pf_spec", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
-        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8),
+        ("kernel", ctypes.c_int32), ("row_prefetch", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
+        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("reserved", ctypes.c_int32 * 11),
     ]
 
     def as_dict(self):

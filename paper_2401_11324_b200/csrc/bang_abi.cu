@@ -148,14 +148,12 @@ struct bang_index {
 namespace {
 
 // stats.kernel ids (bang.h)
-enum KernelId { kKGeneric = 0, kKCta = 2, kKPf = 6, kKSplit = 8 };
+enum KernelId { kKGeneric = 0, kKCta = 2, kKSplit = 8 };
 
 struct Plan {
     int variant = kAdcSmemCodebook;
     int kernel = kKGeneric;
     int npl = 2, sub = 0, mv = 0;
-    int pfw = 1;              // search_pf_kernel: prefetch warps
-    bool pf_stage = false;    // search_pf_kernel: next row's code rows staged in smem
     int off_code = 0;
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
@@ -173,9 +171,10 @@ struct Plan {
 //   exact distances, the HBM table, the shared codebook or BANG_KERNEL_WARP
 //     -> search_kernel (one warp per query, every ADC data flow);
 //   16-byte code rows (m = 32 or 48) with the per-query smem table
-//     -> search_pf_kernel when the codes exceed L2 and R > 32 (its prefetch
-//        warps hide the HBM gathers; measured slower when the codes are
-//        L2-resident), else search_cta_kernel;
+//     -> search_split_kernel for an HBM graph and t <= 256 (row warps and
+//        list warps overlap a hop's memory phase with the previous hop's
+//        merge; measured 1.37x search_cta_kernel at C2 and C3), else
+//        search_cta_kernel (host-mapped graphs, longer worklists);
 //   anything else -> search_kernel.
 bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, Plan &pl) {
     const bang_options &o = ix->opts;
@@ -192,14 +191,14 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     const int64_t tab_bytes = (int64_t)ix->m * 256 * 4;
     const bool forced_generic = exact || (flags & (BANG_TABLE_GLOBAL | BANG_CODEBOOK_SMEM)) ||
                                 o.kernel == BANG_KERNEL_WARP;
-    if ((o.kernel == BANG_KERNEL_CTA || o.kernel == BANG_KERNEL_PF || o.kernel == BANG_KERNEL_SPLIT) &&
-        (forced_generic || mv == 0))
+    if ((o.kernel == BANG_KERNEL_CTA || o.kernel == BANG_KERNEL_SPLIT) && (forced_generic || mv == 0))
         return fail(BANG_E_PARAM, "the CTA kernels need m = 32 or 48 with the smem table (m=%d, flags=%d)", ix->m,
                     flags);
     // ---- one CTA per query, row warps + list warps (search_split_kernel)
-    if (!forced_generic && mv > 0 && o.kernel == BANG_KERNEL_SPLIT) {
-        if (ix->row_hdr || t > 256)
-            return fail(BANG_E_PARAM, "search_split_kernel needs an HBM graph and t <= 256 (t=%d)", t);
+    const bool split_ok = ix->placement == BANG_GRAPH_HBM && t <= 256;
+    if (o.kernel == BANG_KERNEL_SPLIT && !split_ok)
+        return fail(BANG_E_PARAM, "search_split_kernel needs an HBM graph and t <= 256 (t=%d)", t);
+    if (!forced_generic && mv > 0 && split_ok && (o.kernel == BANG_KERNEL_SPLIT || o.kernel == BANG_KERNEL_AUTO)) {
         const int spl = rpad <= 64 ? 1 : 2;
         const int srpad = 64 * spl;
         pl.variant = kAdcSmemTable;
@@ -236,23 +235,15 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.slots = pl.ctas;
         return BANG_OK;
     }
-    // ---- one CTA per query (search_cta_kernel / search_pf_kernel)
+    // ---- one CTA per query (search_cta_kernel)
     if (!forced_generic && mv > 0) {
         pl.variant = kAdcSmemTable;
         pl.sub = vsub;
         pl.mv = mv;
         pl.nt = 2 * rpad;
-        const bool pf_auto = (int64_t)ix->n * ix->m > (int64_t)ix->l2_bytes;
-        pl.pfw = o.pf_warps == 1 || o.pf_warps == 2 ? o.pf_warps : (t <= 4 * (pl.nt - 64) ? 2 : 1);
-        const bool pf_ok = !ix->row_hdr && pl.nt >= 128 && t <= 4 * (pl.nt - 32 * pl.pfw) &&
-                           pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, false);
-        if (o.kernel == BANG_KERNEL_PF && !pf_ok)
-            return fail(BANG_E_PARAM, "search_pf_kernel needs an HBM graph, 32 < R <= 128 and t <= %d (t=%d)",
-                        4 * (pl.nt - 32 * pl.pfw), t);
-        const bool pf = o.kernel == BANG_KERNEL_PF || (o.kernel == BANG_KERNEL_AUTO && pf_auto && pf_ok);
-        if (!pf && t > 4 * 2 * rpad)
+        if (t > 4 * 2 * rpad)
             return fail(BANG_E_PARAM, "t=%d exceeds the CTA kernel's worklist limit %d", t, 8 * rpad);
-        pl.kernel = pf ? kKPf : kKCta;
+        pl.kernel = kKCta;
         int off = 0;
         auto take = [&](int64_t bytes) { const int o_ = off; off += (int)align_up(bytes, 16); return o_; };
         pl.off_q = take(4LL * ix->dim);
@@ -261,32 +252,17 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.off_nk = take(8LL * rpad);
         pl.off_fid = take(4LL * rpad);
         pl.off_alive = take(rpad);
-        pl.off_acc = take(256);  // CtaMisc / PfMisc
+        pl.off_acc = take(256);  // CtaMisc
         pl.off_vis = take(t);
-        // search_pf_kernel clears its filter per query and reads every probe's
-        // word: no summary (its 1.5 KB hold the staged code rows instead)
-        pl.off_sum = pf ? 0 : take(4LL * pl.sum_words);
+        pl.off_sum = take(4LL * pl.sum_words);
         pl.off_tab = take(tab_bytes);
-        if (ix->row_hdr && !pf) pl.off_row = take(4LL * (rpad + 4));
-        if (pf) {
-            // prefetched slots (u32) + pre-state flags (u8)
-            pl.off_dup = take(5LL * pl.nt);
-            // the next row's code rows, staged by the prefetch warps when they fit
-            // the residency search_pf_kernel's launch bounds target (4 CTAs of
-            // 128 threads at m = 48, 6 at m = 32)
-            const int64_t code_bytes = (int64_t)rpad * 16 * pl.mv;
-            const int64_t budget =
-                (int64_t)ix->smem_per_sm / std::max(1, (pl.mv == 3 ? 512 : 768) / pl.nt) - 1024;
-            pl.pf_stage = o.pf_stage != 0 && off + align_up(code_bytes, 16) <= budget;
-            if (pl.pf_stage) pl.off_code = take(code_bytes);
-        }
+        if (ix->row_hdr) pl.off_row = take(4LL * (rpad + 4));
         pl.per_warp = off;  // bytes per CTA
         pl.shared_bytes = 0;
         pl.warps = pl.nt / 32;
         pl.smem = pl.per_warp;
         if (pl.smem > ix->max_smem) return fail(BANG_E_PARAM, "t=%d: %d B of shared memory per query", t, pl.smem);
-        pl.fn = pf ? pick_pf_kernel(pl.nt, pl.sub, pl.mv, pl.pfw, pl.pf_stage)
-                   : pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
+        pl.fn = pick_cta_kernel(pl.nt, pl.sub, pl.mv, ix->row_hdr);
         if (!pl.fn) return fail(BANG_E_STATE, "no CTA kernel for nt=%d sub=%d mv=%d", pl.nt, pl.sub, pl.mv);
         CU(cudaFuncSetAttribute(pl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.smem));
         int per_sm = 0;
@@ -409,7 +385,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     if (ix->bloom.reserve((size_t)pl.slots * pl.bloom_stride)) return BANG_E_OOM;
     if (ix->rr.reserve((size_t)pl.slots * log_cap)) return BANG_E_OOM;
     const bang_options &o = ix->opts;
-    const bool cta = pl.kernel == kKCta || pl.kernel == kKPf || pl.kernel == kKSplit;
+    const bool cta = pl.kernel == kKCta || pl.kernel == kKSplit;
     SearchParams p{};
     p.codes = ix->codes;
     p.code_stride = ix->code_stride;
@@ -468,10 +444,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_tab = pl.off_tab;
     p.off_dup = pl.off_dup;
     p.bloom_clear = o.bloom_clear != 0;
-    p.pf_stage = pl.pf_stage;
     p.off_code = pl.off_code;
-    p.pf_spec = o.pf_spec != 0;
-    p.pf_early = o.pf_early != 0;
+    p.row_prefetch = o.row_prefetch != 0;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -971,10 +945,7 @@ void bang_options_default(bang_options *o) {
     if (!o) return;
     *o = bang_options{};
     o->kernel = BANG_KERNEL_AUTO;
-    o->pf_warps = 0;
-    o->pf_stage = 1;
-    o->pf_early = 1;
-    o->pf_spec = 1;
+    o->row_prefetch = 1;
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;
@@ -982,9 +953,8 @@ void bang_options_default(bang_options *o) {
 
 bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {
     if (!ix || !o) return fail(BANG_E_STATE, "null argument");
-    if (o->kernel < BANG_KERNEL_AUTO || o->kernel > BANG_KERNEL_SPLIT)
+    if (o->kernel < BANG_KERNEL_AUTO || o->kernel > BANG_KERNEL_SPLIT || o->kernel == 3)
         return fail(BANG_E_PARAM, "unknown kernel %d", o->kernel);
-    if (o->pf_warps < 0 || o->pf_warps > 2) return fail(BANG_E_PARAM, "pf_warps must be 0, 1 or 2");
     ix->opts = *o;
     return BANG_OK;
 }

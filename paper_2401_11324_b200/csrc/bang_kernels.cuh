@@ -71,7 +71,7 @@ struct SearchParams {
     int32_t smem_shared_bytes, per_warp_bytes;
     int32_t off_q, off_wl, off_sk, off_nk, off_fid, off_acc, off_alive, off_vis, off_sum, off_tab;  // warp region
     int32_t sum_words;  // u32 words of the Bloom summary (1 bit per filter word)
-    int32_t off_dup;    // search_pf_kernel: prefetched slots + pre-state flags
+    int32_t off_dup;    // search_split_kernel: staged code rows / replay records
     // adjacency row i starts at adj + i * adj_stride.  row_hdr: host-mapped
     // rows carry a 16-byte header [deg, 0, 0, 0] at adj - 4 so one coalesced
     // read fetches degree + ids (search_cta_kernel stages it at off_row)
@@ -80,15 +80,11 @@ struct SearchParams {
     // search_cta_kernel: clear the slot's filter with whole-line stores at
     // query start (else words are zeroed on first touch; bang_options.bloom_clear)
     int32_t bloom_clear;
-    // search_pf_kernel: L2 prefetch of the candidate winners' rows (the head
-    // at expand time, each warp's best fresh neighbour; bang_options.pf_spec)
-    int32_t pf_spec;
-    // search_pf_kernel: the prefetch warps stage the next row's code rows at
-    // off_code (rpad x 16*MV bytes) instead of prefetching them into L2
-    int32_t pf_stage, off_code;
-    // search_pf_kernel: the prefetch warps perform the next row's Bloom sets
-    // (fetch-or) one iteration ahead (bang_options.pf_early)
-    int32_t pf_early;
+    // search_split_kernel: L2 prefetch of the next head's adjacency row, a
+    // candidate for the next winner (bang_options.row_prefetch)
+    int32_t row_prefetch;
+    // search_split_kernel: the row keys (double-buffered) at off_code
+    int32_t off_code;
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
     // one DRAM burst per gathered row)
     int32_t code_stride;

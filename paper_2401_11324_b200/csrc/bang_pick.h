@@ -8,8 +8,6 @@ namespace bang {
 const void *pick_kernel(int npl, int sub, int mv);
 // search_cta_kernel<NT, SUB, MV, HDR> (search_cta.cu)
 const void *pick_cta_kernel(int nt, int sub, int mv, bool hdr);
-// search_pf_kernel<NT, SUB, MV, PFW, STAGE> (search_pf.cu)
-const void *pick_pf_kernel(int nt, int sub, int mv, int pfw, bool stage);
 // search_split_kernel<PL, SUB, MV> (search_split.cu), PL = neighbour slots per row thread
 const void *pick_split_kernel(int pl, int sub, int mv);
 }  // namespace bang

@@ -25,7 +25,7 @@
 // Semantics are SURVEY.md 8(a0) bit for bit (same as search_cta_kernel).
 #pragma once
 
-#include "bang_search_pf.cuh"  // named barriers, L2 row prefetch, clock_after
+#include "bang_search_cta.cuh"
 
 namespace bang {
 
@@ -46,7 +46,24 @@ struct SplitMisc {
 };
 static_assert(sizeof(SplitMisc) <= 256, "SplitMisc must fit its 256-byte smem slot");
 
+// named barrier over a subset of the CTA's warps
 __device__ __forceinline__ void split_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// adjacency row + degree of node v towards L2 (a candidate for the next
+// winner, PAPER.md:922-938 one hop ahead)
+__device__ __forceinline__ void prefetch_row_l2(const SearchParams &p, uint32_t v) {
+    const int32_t *row = p.adj + (int64_t)v * p.adj_stride;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(row) : "memory");
+    if (((uintptr_t)row & 127u) + 4u * (uint32_t)p.R > 128u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(row + p.R - 1) : "memory");
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.deg + v) : "memory");
+}
+// clock64 read that waits for v (a value loaded earlier): the profiler's
+// stamps must depend on the use they time
+__device__ __forceinline__ long long clock_after(int v) {
+    long long c;
+    asm volatile("{\n\t.reg .u32 t;\n\tmov.u32 t, %1;\n\tmov.u64 %0, %%clock64;\n\t}" : "=l"(c) : "r"(v) : "memory");
+    return c;
+}
 
 // 16 bytes of a code row; read-only for the kernel's lifetime, used once
 __device__ __forceinline__ uint4 ldg_code16(const uint8_t *p) {
@@ -85,10 +102,11 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         nid[r] = jj < p.R ? (uint32_t)__ldg(p.adj + (int64_t)w * p.adj_stride + jj) : 0u;
     }
     SPLIT_STAMP(0, nid[0] ^ (uint32_t)deg)
-    // ---- the Bloom pre-state loads (L2), then the code-row gathers (HBM)
-    // staged into shared memory by cp.async: their completion is tracked
-    // apart from the Bloom words', so the Bloom test and the row's sets do
-    // not wait for HBM
+    // ---- the Bloom slots and pre-state words (L2), then the code-row
+    // gathers (HBM) staged into shared memory by cp.async.  The copies'
+    // completion is tracked apart from the Bloom words', so the Bloom test
+    // and the row's sets do not wait for HBM (issuing the copies first was
+    // measured 7% slower: the Bloom words are the longer chain).
     uint32_t p1[PL], p2[PL], wd1[PL], wd2[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
@@ -212,8 +230,9 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     const uint32_t mhi = __reduce_min_sync(kFull, (uint32_t)(mn >> 32));
     const uint32_t mlo = __reduce_min_sync(kFull, (uint32_t)(mn >> 32) == mhi ? (uint32_t)mn : 0xFFFFFFFFu);
     fc = __reduce_add_sync(kFull, fc);
+    const uint64_t wmin = ((uint64_t)mhi << 32) | mlo;
     if (lane == 0) {
-        s_m->rmin[par][rw] = ((uint64_t)mhi << 32) | mlo;
+        s_m->rmin[par][rw] = wmin;
         s_m->rfresh[par][rw] = fc;
     }
     if (rt == 0) s_m->rdeg[par] = deg;
@@ -379,7 +398,7 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         s_m->thr[nxt] = ncnt == t ? last : kSentinel;
         s_m->cnt[nxt] = ncnt;
         // the head may be the next winner: its row to L2
-        if (p.pf_spec && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
+        if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
     }
     SPLIT_STAMP(4, 0)
 #undef SPLIT_STAMP

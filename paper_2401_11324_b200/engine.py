@@ -211,8 +211,8 @@ class DeviceIndex:
 
     def set_options(self, kernel: str = "auto", **tuning) -> None:
         """bang_index_set_options: kernel in _lib.KERNEL_CHOICES plus the
-        bang_options tuning fields (pf_warps, pf_stage, pf_early, pf_spec,
-        bloom_clear, l2_persist, profile); unnamed fields keep their defaults."""
+        bang_options tuning fields (row_prefetch, bloom_clear, l2_persist,
+        profile); unnamed fields keep their defaults."""
         if kernel not in _lib.KERNEL_CHOICES:
             raise ParameterError(f"unknown kernel {kernel!r}; expected one of {sorted(_lib.KERNEL_CHOICES)}")
         o = _lib.Options()
@@ -369,7 +369,7 @@ class GraphSearcher(BaseEstimator):
         return self
 
     def set_kernel(self, kernel: str = "auto", **tuning) -> "GraphSearcher":
-        """Pick the search kernel ("auto", "warp", "cta", "pf", "split") and its tuning
+        """Pick the search kernel ("auto", "warp", "cta", "split") and its tuning
         (bang_options in include/bang.h).  Results are identical for every
         choice; this only moves work between warps and memory levels."""
         self._kernel_options = dict(kernel=kernel, **tuning)

@@ -61,7 +61,8 @@ def test_c1_oracle_matches_reference(t):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("t", [48, 152])
-@pytest.mark.parametrize("kernel,variant", [("auto", "auto"), ("warp", "smem-table"), ("warp", "codebook")])
+@pytest.mark.parametrize("kernel,variant", [("auto", "auto"), ("cta", "auto"), ("warp", "smem-table"),
+                                            ("warp", "codebook")])
 def test_c1_gpu_matches_reference(t, kernel, variant):
     B = pytest.importorskip("paper_2401_11324_b200")
     g = c1()
@@ -80,4 +81,4 @@ def test_c1_gpu_matches_reference(t, kernel, variant):
     assert np.array_equal(res.dists, want_d)
     assert np.array_equal(res.short, want_short)
     if kernel == "auto":
-        assert s.last_stats()["kernel"] == 2  # R = 32, codes fit L2: search_cta_kernel
+        assert s.last_stats()["kernel"] == 8  # HBM graph, m = 32: search_split_kernel

@@ -373,16 +373,11 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     vec = m in (32, 48)
     if vec:
         s.set_adc_variant("auto").set_kernel("auto").search(q[:4])
-        assert s.last_stats()["kernel"] == 2  # CTA per query with the smem table (codes fit L2)
+        assert s.last_stats()["kernel"] == 8  # row + list warps per query, smem table (HBM graph)
     for variant, kernel in _VARIANTS:
         if kernel == "cta" and not vec:
             continue
         res = s.set_adc_variant(variant).set_kernel(kernel).search(q)
-        _same_as_oracle(res, want)
-    if vec and R > 32:
-        # the prefetching kernel (default when the codes exceed L2)
-        res = s.set_adc_variant("auto").set_kernel("pf").search(q)
-        assert s.last_stats()["kernel"] == 6
         _same_as_oracle(res, want)
     if vec:
         res = s.set_adc_variant("auto").set_kernel("split").search(q)
@@ -390,40 +385,34 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
         _same_as_oracle(res, want)
 
 
-# search_pf_kernel data flows: (prefetch warps, staged code rows, early Bloom sets)
-_PF_FLOWS = [(1, 1, 1), (2, 1, 1), (2, 0, 1), (2, 1, 0), (1, 0, 0)]
-
-
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype,z", [
     (16, 16_000, 96, 64, 48, 64, np.float32, 251),
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split"] + [f"pf{w}{s}{e}" for w, s, e in _PF_FLOWS])
+@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch"])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
     """CTA kernels with small Bloom filters: most rows share slots, so the
     warp replay from pre-state bits (replay_row_warp) runs constantly.
     cta: search_cta_kernel (filter cleared per query; -summary: smem bitmap of
-    written words instead); pfWSE: search_pf_kernel with W prefetch warps,
-    staged (S=1) or L2-prefetched code rows, early (E=1) or late Bloom sets."""
+    written words instead); split: search_split_kernel (with and without the
+    head-row L2 prefetch)."""
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     if flow.startswith("cta"):
         s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
-    elif flow == "split":
-        s.set_kernel("split")
     else:
-        w, st, e = (int(c) for c in flow[2:])
-        s.set_kernel("pf", pf_warps=w, pf_stage=st, pf_early=e)
+        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1)
     want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
-    assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8 if flow == "split" else 6)
+    assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8)
     _same_as_oracle(res, want)
 
 
 # ---- the benchmarked operating point's code paths (VERDICT r1: merge chunks
-# c >= 1 of search_pf_kernel at t > NC and of search_cta_kernel at t > NT)
+# c >= 1 of the split kernel's list warps at t > 64 and of search_cta_kernel
+# at t > NT)
 # on C3-shaped indexes of 100K nodes (10M x 96 f32 shape, R=64, m=48) and a
 # C2-shaped one (128-d u8, m=32)
 
@@ -448,21 +437,6 @@ def _big_oracle(shape, t, z=399_887):
         base, q, graph, cb, codes = _big_case(shape)
         _ORACLE[key] = _oracle_search(q, graph, cb, codes, base, t, z)
     return _ORACLE[key]
-
-
-@pytest.mark.parametrize("t", [100, 166, 256])
-@pytest.mark.parametrize("pfw,stage,early", [(2, 1, 1), (1, 1, 1), (2, 0, 1), (2, 1, 0)])
-def test_pf_kernel_large_t_matches_oracle(t, pfw, stage, early):
-    """search_pf_kernel at worklists spanning 2-4 merge chunks of NC = 64/96
-    threads (t=166 is the C3 benchmark's operating point)."""
-    base, q, graph, cb, codes = _big_case("C3")
-    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
-    s.fit(base, graph=graph, codebook=cb, codes=codes)
-    s.set_kernel("pf", pf_warps=pfw, pf_stage=stage, pf_early=early)
-    res = s.search(q)
-    st = s.last_stats()
-    assert st["kernel"] == 6
-    _same_as_oracle(res, _big_oracle("C3", t))
 
 
 @pytest.mark.parametrize("shape,t", [("C3", 100), ("C3", 166), ("C3", 256), ("C2", 80), ("C2", 200)])
@@ -494,7 +468,7 @@ def test_wide_and_narrow_rows_match_oracle(seed, n, d, R, m, t, dtype):
 
 
 @pytest.mark.parametrize("t,k", [(1, 1), (10, 10), (11, 10)])
-@pytest.mark.parametrize("kernel", ["split", "cta", "pf"])
+@pytest.mark.parametrize("kernel", ["split", "cta"])
 def test_cta_kernels_tiny_worklists_match_oracle(t, k, kernel):
     """t = k down to 1: the threshold is the single entry, heads run out at once."""
     base, q, graph, cb, codes = _random_case(26, 8_000, 96, 64, 48, 100, np.float32)
@@ -506,7 +480,7 @@ def test_cta_kernels_tiny_worklists_match_oracle(t, k, kernel):
         _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, t, rerank=rerank, k=k))
 
 
-@pytest.mark.parametrize("kernel", ["split", "pf", "cta"])
+@pytest.mark.parametrize("kernel", ["split", "cta"])
 def test_cta_kernels_without_rerank_match_oracle(kernel):
     """rerank=False: the outputs are the final worklist's first k entries."""
     base, q, graph, cb, codes = _big_case("C3")
@@ -527,16 +501,6 @@ def test_cta_kernel_large_t_matches_oracle(shape, t):
     _same_as_oracle(res, _big_oracle(shape, t))
 
 
-def test_pf_kernel_c2_shape_matches_oracle():
-    """search_pf_kernel over 32-byte code rows (m = 32, sub = 4) at t = 200."""
-    base, q, graph, cb, codes = _big_case("C2")
-    s = B.GraphSearcher(k=10, t=200, mode="in_memory", bloom_entries=399_887, debug_checks=True)
-    s.fit(base, graph=graph, codebook=cb, codes=codes)
-    res = s.set_kernel("pf").search(q)
-    assert s.last_stats()["kernel"] == 6
-    _same_as_oracle(res, _big_oracle("C2", 200))
-
-
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
     (14, 16_000, 128, 64, 32, 48, np.uint8),
     (15, 16_000, 96, 64, 48, 64, np.float32),
@@ -553,7 +517,7 @@ def test_pipelined_cta_kernel_matches_oracle(seed, n, d, R, m, t, dtype):
     _same_as_oracle(res, want)
 
 
-@pytest.mark.parametrize("kernel", ["cta", "pf", "split"])
+@pytest.mark.parametrize("kernel", ["cta", "split"])
 def test_cta_kernels_overflow_retry_is_exact(kernel):
     from paper_2401_11324_b200 import _lib
     base, q, graph, cb, codes = _random_case(10, 16_000, 96, 64, 48, 200, np.float32)
