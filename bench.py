@@ -576,7 +576,7 @@ def main():
         it = max(1, s_last["iterations"])
         if s_last.get("kernel") == 8:  # search_split_kernel: row thread 0 / list thread 0 per hop
             prof = searcher.index_.options().get("profile", 0)
-            names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "fetch_or_back", "coll_bar", "row_end"],
+            names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "hashed", "coll_bar", "row_end"],
                      3: ["compact", "sort", "merge_reads", "merge_writes", "list_end"]}.get(
                 prof, ["row_chain", "list_step", "row_wait_at_hop_barrier", "list_wait_at_hop_barrier"])
             out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -195,9 +196,9 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         return fail(BANG_E_PARAM, "the CTA kernels need m = 32 or 48 with the smem table (m=%d, flags=%d)", ix->m,
                     flags);
     // ---- one CTA per query, row warps + list warps (search_split_kernel)
-    const bool split_ok = ix->placement == BANG_GRAPH_HBM && t <= 256;
+    const bool split_ok = t <= 256;
     if (o.kernel == BANG_KERNEL_SPLIT && !split_ok)
-        return fail(BANG_E_PARAM, "search_split_kernel needs an HBM graph and t <= 256 (t=%d)", t);
+        return fail(BANG_E_PARAM, "search_split_kernel needs t <= 256 (t=%d)", t);
     if (!forced_generic && mv > 0 && split_ok && (o.kernel == BANG_KERNEL_SPLIT || o.kernel == BANG_KERNEL_AUTO)) {
         const int spl = rpad <= 64 ? 1 : 2;
         const int srpad = 64 * spl;
@@ -395,7 +396,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.table = d_table;
     p.adj = ix->adj;
     p.adj_stride = ix->adj_stride;
-    p.row_hdr = ix->row_hdr && pl.kernel == kKCta ? 1 : 0;
+    p.row_hdr = ix->row_hdr ? 1 : 0;
+    p.host_graph = ix->host_graph ? 1 : 0;
     p.off_row = pl.off_row;
     p.deg = ix->deg;
     p.vectors = ix->vectors;
@@ -446,6 +448,8 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
+    p.vec_prefetch = o.vec_prefetch != 0;
+    p.adc_early_exit = o.adc_early_exit != 0;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -698,12 +702,20 @@ bang_status bang_index_create(int32_t device, const uint8_t *codes, int64_t n, i
         CUX(cudaHostAlloc(&ix->vectors, vec_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
         ix->adj = ix->adj_alloc + (ix->row_hdr ? 4 : 0);
         if (ix->row_hdr) {
-            for (int64_t i = 0; i < n; ++i) {
-                int32_t *row = ix->adj_alloc + i * ix->adj_stride;
-                row[0] = degrees[i];
-                row[1] = row[2] = row[3] = 0;
-                memcpy(row + 4, adjacency + i * R, (size_t)R * 4);
-            }
+            // header + row per node, written by all host threads (27 GB at 100M x 64)
+            const int T = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+            auto fill = [&](int tix) {
+                for (int64_t i = n * tix / T; i < n * (tix + 1) / T; ++i) {
+                    int32_t *row = ix->adj_alloc + i * ix->adj_stride;
+                    row[0] = degrees[i];
+                    row[1] = row[2] = row[3] = 0;
+                    memcpy(row + 4, adjacency + i * R, (size_t)R * 4);
+                }
+            };
+            std::vector<std::thread> pool;
+            for (int tix = 1; tix < T; ++tix) pool.emplace_back(fill, tix);
+            fill(0);
+            for (auto &th : pool) th.join();
         } else {
             memcpy(ix->adj, adjacency, adj_bytes);
         }
@@ -946,6 +958,8 @@ void bang_options_default(bang_options *o) {
     *o = bang_options{};
     o->kernel = BANG_KERNEL_AUTO;
     o->row_prefetch = 1;
+    o->vec_prefetch = 1;
+    o->adc_early_exit = 1;
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;

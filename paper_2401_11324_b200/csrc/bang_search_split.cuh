@@ -77,14 +77,43 @@ __device__ __forceinline__ uint32_t u4_word(const uint4 &v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
+// warp_topk_write over keys in shared memory: k rounds of "smallest key
+// above the last one" (keys are unique), ids -1 / dists +inf padded
+__device__ __forceinline__ void warp_topk_write_smem(const uint64_t *keys, int L, int k, int32_t *out_ids,
+                                                     float *out_dists) {
+    const int lane = (int)lane_id();
+    uint64_t last = 0;
+    for (int j = 0; j < k; ++j) {
+        uint64_t local = kSentinel;
+        if (j < L)
+            for (int i = lane; i < L; i += 32) {
+                const uint64_t v = keys[i];
+                if ((j == 0 || v > last) && v < local) local = v;
+            }
+        const uint64_t sel = warp_min_u64(local);
+        if (lane == 0) {
+            out_ids[j] = sel != kSentinel ? (int32_t)key_id(sel) : -1;
+            out_dists[j] = sel != kSentinel ? key_dist(sel) : __int_as_float(0x7f800000);
+        }
+        last = sel;
+    }
+}
+
 // Row warps: the row of node w -> keys in s_key[0, 64*PL) (SENTINEL for
 // slots past the degree and for neighbours the Bloom filter drops); their
 // minimum and fresh count in s_m (parity `par`).  rt = thread index among
 // the 64 row threads.
+//
+// thr_prev: the truncation threshold of the hop that chose w.  Thresholds
+// only fall (merging smaller keys lowers the t-th smallest), so a neighbour
+// whose partial sum already exceeds it can neither survive the merge nor be
+// the eager winner (the head, <= the threshold, beats it): its ADC stops
+// there and its key is the partial sum, which still compares >= every
+// later threshold.
 template <int PL, int MV>
 __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int rt, const float *s_tab,
                                           uint32_t *bits, uint64_t *s_key, SplitMisc *s_m, int par,
-                                          uint8_t *s_stage, uint8_t *s_tf) {
+                                          uint8_t *s_stage, uint8_t *s_tf, uint64_t thr_prev) {
     constexpr int M = 16 * MV;
     constexpr int RPAD = 64 * PL;
     constexpr int CH = 16;  // table lookups issued ahead of their sums
@@ -94,12 +123,19 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     const long long c0 = bk ? clock64() : 0;
 #define SPLIT_STAMP(slot, dep) \
     if (bk) s_m->ph[slot] += (unsigned long long)(clock_after((int)(dep)) - c0);
-    const int deg = __ldg(p.deg + w);
+    const int32_t *row = p.adj + (int64_t)w * p.adj_stride;
     uint32_t nid[PL];
+    int deg;
+    if (p.host_graph) {
+        // pinned, mapped host rows read over PCIe; with a [deg, 0, 0, 0]
+        // header (p.row_hdr) degree and ids come in one coalesced read
+        deg = p.row_hdr ? row[-4] : p.deg[w];
 #pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        const int jj = rt + 64 * r;
-        nid[r] = jj < p.R ? (uint32_t)__ldg(p.adj + (int64_t)w * p.adj_stride + jj) : 0u;
+        for (int r = 0; r < PL; ++r) nid[r] = rt + 64 * r < p.R ? (uint32_t)row[rt + 64 * r] : 0u;
+    } else {
+        deg = __ldg(p.deg + w);
+#pragma unroll
+        for (int r = 0; r < PL; ++r) nid[r] = rt + 64 * r < p.R ? (uint32_t)__ldg(row + rt + 64 * r) : 0u;
     }
     SPLIT_STAMP(0, nid[0] ^ (uint32_t)deg)
     // ---- the Bloom slots and pre-state words (L2), then the code-row
@@ -114,6 +150,12 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         if (rt + 64 * r < deg) {
             p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
             p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
+        }
+    }
+    SPLIT_STAMP(4, p1[0] ^ p2[0])
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        if (rt + 64 * r < deg) {
             wd1[r] = __ldcg(bits + (p1[r] >> 5));
             wd2[r] = __ldcg(bits + (p2[r] >> 5));
         }
@@ -155,6 +197,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     // acc = ((0 + T[0][c0]) + T[1][c1]) + ... in f32 (engine.py:99-105); the
     // lookups of a chunk are issued before its sums
     __pipeline_wait_prior(0);  // this thread's own staged rows
+    // (SENTINEL's high word is a NaN: no exit while the worklist is not full)
+    const float tdist = key_dist(thr_prev);
     float acc[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
@@ -166,6 +210,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
                 code[v] = *reinterpret_cast<const uint4 *>(s_stage + (rt + 64 * r) * M + 16 * v);
 #pragma unroll
             for (int s0 = 0; s0 < M; s0 += CH) {
+                if (p.adc_early_exit && s0 > 0 && acc[r] > tdist) break;
                 float e[CH];
 #pragma unroll
                 for (int q = 0; q < CH; ++q) {
@@ -189,7 +234,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         sh2[r] = pf[r] && p2[r] != p1[r] && !b2[r] && ((o2[r] >> (p2[r] & 31)) & 1u);
         any_sh = any_sh || sh1[r] || sh2[r];
     }
-    SPLIT_STAMP(4, any_sh)
     if (any_sh) s_m->coll = 1;
     split_bar(3, 64);
     SPLIT_STAMP(5, 0)
@@ -393,6 +437,14 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         }
         if (wpos < t) s_vis[wpos] = 1;
         if (iters < p.log_cap) log[iters] = (int32_t)key_id(winner);
+        // the re-rank reads this node's vector after the search: ask L2 for
+        // it now, while the hop's HBM traffic is the codes'
+        if (p.vec_prefetch) {
+            const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
+            const uint8_t *v = static_cast<const uint8_t *>(p.vectors) + (int64_t)key_id(winner) * rowb;
+            for (int b = 0; b < rowb; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(v + b) : "memory");
+            if (((uintptr_t)v & 127u) + (rowb & 127) > 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(v + rowb - 1) : "memory");
+        }
         s_m->hpos[nxt] = hp;
         s_m->head[nxt] = hk;
         s_m->thr[nxt] = ncnt == t ? last : kSentinel;
@@ -453,7 +505,9 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
         }
         __syncthreads();
-        // kernel 1 for this query into shared memory (pq.py:284-296)
+        // kernel 1 for this query into shared memory (pq.py:284-296); the
+        // centroid loads (L2) of 8 entries per thread are in flight together
+#pragma unroll 8
         for (int idx = tid; idx < M * 256; idx += NT) {
             const int s = idx >> 8, c = idx & 255;
             float e;
@@ -501,7 +555,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
             s_m->cnt[0] = 1;
         }
-        if (roww) split_row<PL, MV>(p, (uint32_t)p.medoid, tid, s_tab, bits, s_key, s_m, 0, s_stage, s_tf);
+        if (roww) split_row<PL, MV>(p, (uint32_t)p.medoid, tid, s_tab, bits, s_key, s_m, 0, s_stage, s_tf, kSentinel);
         if (p.profile && tid == 0) {
             const long long now_ = clock64();
             s_m->ph[7] += (unsigned long long)(now_ - c_q);
@@ -521,7 +575,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             const long long c0 = prof ? clock64() : 0;
             if (roww) {
                 split_row<PL, MV>(p, key_id(winner), tid, s_tab, bits, s_key + (par ^ 1) * RPAD, s_m, par ^ 1,
-                                  s_stage, s_tf);
+                                  s_stage, s_tf, thr);
             } else {
                 split_list<PL>(p, tid - 64, s_wl, s_vis, s_key + par * RPAD, s_nk, s_sk, s_c, s_spos, s_m, par ^ 1,
                                winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters);
@@ -560,6 +614,22 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             __threadfence_block();
             __syncthreads();
             const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
+            const int tab_b = M * 256 * 4, kb = (8 * iters + 15) & ~15;
+            if (rowb % 16 == 0 && kb <= tab_b / 2 && rowb <= tab_b - kb) {
+                // the table is dead until the next query: stage rows in its
+                // place and keep the keys at its end, so the top-k reads
+                // shared memory
+                uint64_t *s_rr = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(s_tab) + tab_b - kb);
+                rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), tab_b - kb, s_rr);
+                st_rr += (tid == 0) ? iters : 0;
+                if (tid < 32) {
+                    warp_topk_write_smem(s_rr, iters, p.k, oid, odist);
+                    if (tid == 0) p.out_short[qid] = iters < p.k;
+                }
+                __syncthreads();
+                if (p.profile && tid == 0) s_m->ph[7] += (unsigned long long)(clock64() - c_q);
+                continue;
+            }
             if (rowb % 16 == 0 && rowb <= M * 256 * 4) {
                 // the table is dead until the next query: stage rows in its place
                 rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), M * 256 * 4, rr);
