@@ -549,6 +549,32 @@ def main():
                 "adc_bytes": s_last["adc_bytes"],
                 "adc_gbs": round(s_last["adc_bytes"] / (avg_kern_ms / 1000.0) / 1e9, 1)}
 
+    if thr_only:
+        # host-resident graph (mode="pipelined"): rows and re-rank vectors
+        # cross PCIe; the bound is the measured zero-copy read rate of random
+        # rows of the same size (bang_host_read_bandwidth, mode 1)
+        import ctypes
+        R, d = meta["R"], meta["dim"]
+        elem = 1 if meta["dtype"] == "u8" else 4
+        row_b = 4 * (R + 4) if R % 4 == 0 else 4 * R
+        host_bytes = s_last["iterations"] * row_b + s_last["rerank_cands"] * d * elem
+        gbs = ctypes.c_double()
+        _lib.check(_lib.lib().bang_host_read_bandwidth(local, 1 << 30, 1, (row_b + 15) // 16 * 16, ctypes.byref(gbs)),
+                   "bang_host_read_bandwidth")
+        stream_gbs = ctypes.c_double()
+        _lib.check(_lib.lib().bang_host_read_bandwidth(local, 1 << 30, 0, 16, ctypes.byref(stream_gbs)),
+                   "bang_host_read_bandwidth")
+        host_ach = host_bytes / (avg_kern_ms / 1000.0) / 1e9
+        roofline["hbm_bound"] = {k2: roofline[k2] for k2 in ("achieved", "peak", "frac")}
+        roofline.update({"bound": "pcie", "achieved": round(host_ach, 2), "peak": round(gbs.value, 2),
+                         "frac": round(host_ach / gbs.value, 4), "peak_kind": "measured",
+                         "peak_source": f"bang_host_read_bandwidth: random {(row_b + 15) // 16 * 16}-byte rows of "
+                                        f"pinned mapped host memory (1 GiB), one warp per row",
+                         "pcie_stream_gbs": round(stream_gbs.value, 2),
+                         "host_bytes": int(host_bytes),
+                         "host_bytes_formula": f"I x {row_b} (row with [deg,0,0,0] header) + C x {d * elem} "
+                                               f"(re-rank vectors)"})
+
     # ---- kernel 3 on its own (north_star "ADC kernel HBM GB/s vs peak",
     # SURVEY.md 8(d)): every (query, neighbour) probe of this benchmark's
     # searches, grouped by query, through bang_adc_pairs_device
@@ -576,7 +602,7 @@ def main():
         it = max(1, s_last["iterations"])
         if s_last.get("kernel") == 8:  # search_split_kernel: row thread 0 / list thread 0 per hop
             prof = searcher.index_.options().get("profile", 0)
-            names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "hashed", "coll_bar", "row_end"],
+            names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "unused", "coll_bar", "row_end"],
                      3: ["compact", "sort", "merge_reads", "merge_writes", "list_end"]}.get(
                 prof, ["row_chain", "list_step", "row_wait_at_hop_barrier", "list_wait_at_hop_barrier"])
             out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}

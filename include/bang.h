@@ -76,10 +76,7 @@ typedef struct bang_options {
     int32_t l2_persist;   /* 1: the Bloom filters get an L2-persisting access window      */
     int32_t profile;      /* with BANG_PROFILE_PHASES: 2 = search_split_kernel's row-warp
                              stages, 3 = its list-warp stages                            */
-    int32_t vec_prefetch; /* 1: L2 prefetch of each expanded node's re-rank vector (split) */
-    int32_t adc_early_exit; /* 1: a neighbour's ADC stops once its partial sum exceeds the
-                               hop's truncation threshold (it can neither survive nor win) */
-    int32_t reserved[9];
+    int32_t reserved[11];
 } bang_options;
 
 typedef struct bang_index bang_index;
@@ -202,6 +199,13 @@ bang_status bang_sync_status(bang_index *index);
 bang_status bang_read_graph_header(const char *path, int64_t *n, int32_t *R, int32_t *medoid);
 bang_status bang_read_graph(const char *path, int32_t *adjacency, int32_t *degrees, int64_t n, int32_t R,
                             int32_t threads);
+
+/* PCIe roofline of the host-resident graph path (diagnostic, no handle):
+ * GB/s a kernel reads from `bytes` of pinned, mapped host memory -- mode 0
+ * streaming, mode 1 random rows of row_bytes, one warp per row (the search's
+ * zero-copy row fetch).  The reference has no counterpart (its graph is in
+ * host RAM by construction); bench.py reports the host path against it. */
+bang_status bang_host_read_bandwidth(int32_t device, int64_t bytes, int32_t mode, int32_t row_bytes, double *gbs);
 
 /* ---------------------------------------------- per-kernel entries (device pointers) */
 

@@ -49,8 +49,8 @@ class Options(ctypes.Structure):
     """bang_options (include/bang.h): per-index kernel choice and tuning."""
     _fields_ = [
         ("kernel", ctypes.c_int32), ("row_prefetch", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
-        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("vec_prefetch", ctypes.c_int32),
-        ("adc_early_exit", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9),
+        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 11),
     ]
 
     def as_dict(self):
@@ -108,6 +108,7 @@ _SIGS = {
     "bang_worklist_update_device": (_I32, [_P, _P, _I64, _I32, _P, _I32, _P, _P, _P]),
     "bang_rerank_device": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P, _I32, _P, _P, _P, _P]),
     "bang_exact_sq_dists_device": (_I32, [_P, _I32, _I32, _P, _I64, _P, _P]),
+    "bang_host_read_bandwidth": (_I32, [_I32, _I64, _I32, _I32, ctypes.POINTER(ctypes.c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

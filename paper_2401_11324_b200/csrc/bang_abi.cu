@@ -448,8 +448,6 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
-    p.vec_prefetch = o.vec_prefetch != 0;
-    p.adc_early_exit = o.adc_early_exit != 0;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -585,6 +583,34 @@ bang_status collect(bang_index *ix, unsigned long long *ctr) {
 }
 
 }  // namespace
+
+// ---- PCIe read roofline for the host-resident graph path (diagnostic):
+// streaming (mode 0: each thread reads consecutive 16-byte pieces) or random
+// rows of row_bytes (mode 1: one warp per row, the search's access pattern)
+// from pinned, mapped host memory
+__global__ void host_read_kernel(const uint4 *__restrict__ src, int64_t n16, int mode, int row16, int64_t nrows,
+                                 int64_t reads, unsigned long long *sink) {
+    uint32_t acc = 0;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    if (mode == 0) {
+        for (int64_t i = tid; i < n16; i += nt) {
+            const uint4 v = src[i];
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    } else {
+        const int64_t warp = tid >> 5, nw = nt >> 5;
+        const int lane = threadIdx.x & 31;
+        for (int64_t r = warp; r < reads; r += nw) {
+            const uint64_t h = (uint64_t)r * 0x9E3779B97F4A7C15ull;
+            const int64_t row = (int64_t)((h >> 17) % (uint64_t)nrows);
+            if (lane < row16) {
+                const uint4 v = src[row * row16 + lane];
+                acc ^= v.x ^ v.y ^ v.z ^ v.w;
+            }
+        }
+    }
+    if (acc == 0x9E3779B9u) atomicAdd(sink, 1ull);  // keeps the loads
+}
 
 extern "C" {
 
@@ -958,8 +984,6 @@ void bang_options_default(bang_options *o) {
     *o = bang_options{};
     o->kernel = BANG_KERNEL_AUTO;
     o->row_prefetch = 1;
-    o->vec_prefetch = 1;
-    o->adc_early_exit = 1;
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;
@@ -1153,6 +1177,50 @@ bang_status bang_exact_sq_dists_device(const void *d_points, int32_t vec_dtype, 
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     exact_dists_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>(d_points, vec_dtype, dim, d_queries, n, d_out);
     CU(cudaGetLastError());
+    return BANG_OK;
+}
+
+bang_status bang_host_read_bandwidth(int32_t device, int64_t bytes, int32_t mode, int32_t row_bytes, double *gbs) {
+    if (!gbs || bytes < (1 << 20) || (mode != 0 && mode != 1) || (mode == 1 && (row_bytes < 16 || row_bytes > 512 ||
+                                                                                row_bytes % 16)))
+        return fail(BANG_E_PARAM, "bytes >= 1 MiB, mode 0/1, row_bytes a multiple of 16 in [16, 512]");
+    CU(cudaSetDevice(device));
+    void *h = nullptr;
+    unsigned long long *sink = nullptr;
+    CU(cudaHostAlloc(&h, (size_t)bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(h, 1, (size_t)bytes);
+    void *d = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&d, h, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&sink, sizeof(unsigned long long));
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (e == cudaSuccess) e = cudaEventCreate(&a);
+    if (e == cudaSuccess) e = cudaEventCreate(&b);
+    float ms = 0.0f;
+    int64_t moved = 0;
+    if (e == cudaSuccess) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        const int64_t n16 = bytes / 16, row16 = row_bytes / 16, nrows = bytes / (row_bytes ? row_bytes : 16);
+        const int64_t reads = mode == 1 ? nrows : 0;
+        moved = mode == 0 ? n16 * 16 : reads * row_bytes;
+        for (int it = 0; it < 2 && e == cudaSuccess; ++it) {  // warm-up, then timed
+            cudaEventRecord(a);
+            host_read_kernel<<<sms * 8, 256>>>(static_cast<const uint4 *>(d), n16, mode, (int)row16, nrows, reads,
+                                               sink);
+            cudaEventRecord(b);
+            e = cudaEventSynchronize(b);
+        }
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+    }
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    if (sink) cudaFree(sink);
+    cudaFreeHost(h);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(BANG_E_CUDA, "host read bandwidth: %s", cudaGetErrorString(e));
+    }
+    *gbs = moved / (ms * 1e6);
     return BANG_OK;
 }
 

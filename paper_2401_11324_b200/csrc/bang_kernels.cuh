@@ -83,13 +83,8 @@ struct SearchParams {
     // search_split_kernel: L2 prefetch of the next head's adjacency row, a
     // candidate for the next winner (bang_options.row_prefetch)
     int32_t row_prefetch;
-    // search_split_kernel: L2 prefetch of each expanded node's re-rank vector
-    // (bang_options.vec_prefetch); host_graph: graph + vectors in pinned,
-    // mapped host memory
-    int32_t vec_prefetch, host_graph;
-    // search_split_kernel: stop a neighbour's ADC once its partial sum
-    // exceeds the hop's truncation threshold (bang_options.adc_early_exit)
-    int32_t adc_early_exit;
+    // graph + vectors in pinned, mapped host memory (mode="pipelined")
+    int32_t host_graph;
     // search_split_kernel: the row keys (double-buffered) at off_code
     int32_t off_code;
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:

@@ -44,7 +44,8 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
                                               const float *s_q, uint8_t *stage, int stage_bytes,
                                               uint64_t *rr) {
     const int tid = threadIdx.x;
-    const int rb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);  // a multiple of 16 (caller)
+    const int dim = p.dim, dtype = p.vec_dtype;  // (registers: the stores below may alias p)
+    const int rb = dim * (dtype == kVecF32 ? 4 : 1);  // a multiple of 16 (caller)
     const int upr = rb / 16;
     const int ch = stage_bytes / rb;
     const uint8_t *vec = static_cast<const uint8_t *>(p.vectors);
@@ -58,7 +59,7 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
         __syncthreads();
         for (int i = tid; i < nr; i += NT) {
             const uint32_t node = (uint32_t)__ldcg(log + base + i);
-            rr[base + i] = pack_key(exact_sq_dist(stage, p.vec_dtype, p.dim, i, s_q), node);
+            rr[base + i] = pack_key(exact_sq_dist(stage, dtype, dim, i, s_q), node);
         }
         __syncthreads();
     }

@@ -99,23 +99,52 @@ __device__ __forceinline__ void warp_topk_write_smem(const uint64_t *keys, int L
     }
 }
 
+// Rare path of split_row (~2% of rows at z = 399,887), kept out of line so
+// the hop loop's code stays compact: exact sequential replay of the involved
+// probes by row warp 0 from the pre-state bits; the records go where the
+// (consumed) code rows were staged.  All 64 row threads call it; the probe
+// state travels by value (registers) and the truly fresh flags come back as
+// a bit mask (bit r: slot rt + 64 r).
+template <int PL>
+struct RowProbes {
+    uint32_t p1[PL], p2[PL];
+    uint32_t pf, b1, b2, sh1, sh2;  // bit r: slot rt + 64 r
+};
+template <int PL>
+__device__ __noinline__ uint32_t split_replay(int rt, int deg, const RowProbes<PL> pr, uint8_t *s_stage,
+                                              uint32_t *bits, uint8_t *s_tf) {
+    constexpr int RPAD = 64 * PL;
+    uint2 *s_rec = reinterpret_cast<uint2 *>(s_stage);
+    uint8_t *s_fl2 = s_stage + 8 * RPAD;
+    split_bar(3, 64);  // every row thread has read its staged rows
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        const int jj = rt + 64 * r;
+        const uint32_t m = 1u << r;
+        s_rec[jj] = make_uint2(pr.p1[r], pr.p2[r]);
+        s_fl2[2 * jj] = (uint8_t)((pr.pf & m ? 2 : 0) | (pr.b1 & m ? 4 : 0) | (pr.sh1 & m ? 8 : 0));
+        s_fl2[2 * jj + 1] = (uint8_t)((pr.b2 & m ? 4 : 0) | (pr.sh2 & m ? 8 : 0));
+    }
+    split_bar(3, 64);
+    if ((rt >> 5) == 0) replay_row_warp<RPAD / 32>(s_rec, s_fl2, deg, bits, s_tf);
+    split_bar(3, 64);
+    uint32_t fresh = 0;
+#pragma unroll
+    for (int r = 0; r < PL; ++r)
+        if (rt + 64 * r < deg && s_tf[rt + 64 * r]) fresh |= 1u << r;
+    return fresh;
+}
+
 // Row warps: the row of node w -> keys in s_key[0, 64*PL) (SENTINEL for
 // slots past the degree and for neighbours the Bloom filter drops); their
 // minimum and fresh count in s_m (parity `par`).  rt = thread index among
 // the 64 row threads.
-//
-// thr_prev: the truncation threshold of the hop that chose w.  Thresholds
-// only fall (merging smaller keys lowers the t-th smallest), so a neighbour
-// whose partial sum already exceeds it can neither survive the merge nor be
-// the eager winner (the head, <= the threshold, beats it): its ADC stops
-// there and its key is the partial sum, which still compares >= every
-// later threshold.
+
 template <int PL, int MV>
 __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int rt, const float *s_tab,
                                           uint32_t *bits, uint64_t *s_key, SplitMisc *s_m, int par,
-                                          uint8_t *s_stage, uint8_t *s_tf, uint64_t thr_prev) {
+                                          uint8_t *s_stage, uint8_t *s_tf) {
     constexpr int M = 16 * MV;
-    constexpr int RPAD = 64 * PL;
     constexpr int CH = 16;  // table lookups issued ahead of their sums
     const int rw = rt >> 5, lane = rt & 31;
     // (p.profile == 2) row thread 0's cycles from entry to each stage, per hop
@@ -150,12 +179,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         if (rt + 64 * r < deg) {
             p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
             p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
-        }
-    }
-    SPLIT_STAMP(4, p1[0] ^ p2[0])
-#pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        if (rt + 64 * r < deg) {
             wd1[r] = __ldcg(bits + (p1[r] >> 5));
             wd2[r] = __ldcg(bits + (p2[r] >> 5));
         }
@@ -197,8 +220,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     // acc = ((0 + T[0][c0]) + T[1][c1]) + ... in f32 (engine.py:99-105); the
     // lookups of a chunk are issued before its sums
     __pipeline_wait_prior(0);  // this thread's own staged rows
-    // (SENTINEL's high word is a NaN: no exit while the worklist is not full)
-    const float tdist = key_dist(thr_prev);
     float acc[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
@@ -210,7 +231,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
                 code[v] = *reinterpret_cast<const uint4 *>(s_stage + (rt + 64 * r) * M + 16 * v);
 #pragma unroll
             for (int s0 = 0; s0 < M; s0 += CH) {
-                if (p.adc_early_exit && s0 > 0 && acc[r] > tdist) break;
                 float e[CH];
 #pragma unroll
                 for (int q = 0; q < CH; ++q) {
@@ -241,24 +261,21 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #pragma unroll
     for (int r = 0; r < PL; ++r) fresh[r] = pf[r];
     if (s_m->coll) {
-        // rare (~2% of rows at z = 399,887): exact sequential replay of the
-        // involved probes by row warp 0 from the pre-state bits; the records
-        // go where the (consumed) code rows were staged
-        uint2 *s_rec = reinterpret_cast<uint2 *>(s_stage);
-        uint8_t *s_fl2 = s_stage + 8 * RPAD;
-        split_bar(3, 64);  // every row thread has read its staged rows
+        RowProbes<PL> pr;
+        pr.pf = pr.b1 = pr.b2 = pr.sh1 = pr.sh2 = 0;
 #pragma unroll
         for (int r = 0; r < PL; ++r) {
-            const int jj = rt + 64 * r;
-            s_rec[jj] = make_uint2(p1[r], p2[r]);
-            s_fl2[2 * jj] = (uint8_t)((pf[r] ? 2 : 0) | (b1[r] ? 4 : 0) | (sh1[r] ? 8 : 0));
-            s_fl2[2 * jj + 1] = (uint8_t)((b2[r] ? 4 : 0) | (sh2[r] ? 8 : 0));
+            pr.p1[r] = p1[r];
+            pr.p2[r] = p2[r];
+            pr.pf |= (uint32_t)pf[r] << r;
+            pr.b1 |= (uint32_t)b1[r] << r;
+            pr.b2 |= (uint32_t)b2[r] << r;
+            pr.sh1 |= (uint32_t)sh1[r] << r;
+            pr.sh2 |= (uint32_t)sh2[r] << r;
         }
-        split_bar(3, 64);
-        if (rw == 0) replay_row_warp<RPAD / 32>(s_rec, s_fl2, deg, bits, s_tf);
-        split_bar(3, 64);
+        const uint32_t f = split_replay<PL>(rt, deg, pr, s_stage, bits, s_tf);
 #pragma unroll
-        for (int r = 0; r < PL; ++r) fresh[r] = rt + 64 * r < deg && s_tf[rt + 64 * r];
+        for (int r = 0; r < PL; ++r) fresh[r] = (f >> r) & 1u;
     }
     // keys out; per-warp minimum (dist bits, then id: two 32-bit
     // reductions) and fresh count
@@ -437,14 +454,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         }
         if (wpos < t) s_vis[wpos] = 1;
         if (iters < p.log_cap) log[iters] = (int32_t)key_id(winner);
-        // the re-rank reads this node's vector after the search: ask L2 for
-        // it now, while the hop's HBM traffic is the codes'
-        if (p.vec_prefetch) {
-            const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
-            const uint8_t *v = static_cast<const uint8_t *>(p.vectors) + (int64_t)key_id(winner) * rowb;
-            for (int b = 0; b < rowb; b += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(v + b) : "memory");
-            if (((uintptr_t)v & 127u) + (rowb & 127) > 128u) asm volatile("prefetch.global.L2 [%0];" ::"l"(v + rowb - 1) : "memory");
-        }
         s_m->hpos[nxt] = hp;
         s_m->head[nxt] = hk;
         s_m->thr[nxt] = ncnt == t ? last : kSentinel;
@@ -456,9 +465,142 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
 #undef SPLIT_STAMP
 }
 
-template <int PL, int SUB, int MV>
-__global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(const SearchParams p) {
+// Per-query prologue (all 128 threads): the query, the cleared filter
+// (whole-line stores), kernel 1 into shared memory (pq.py:284-296) and the
+// medoid in the filter (engine.py:127-128).  (Measured 2% faster inline than
+// out of line.)
+template <int SUB, int MV>
+__device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qid, float *s_q, uint8_t *s_vis,
+                                            float *s_tab, uint32_t *bits) {
     constexpr int NT = 128;
+    constexpr int M = 16 * MV;
+    const int tid = threadIdx.x;
+    // parameters in registers: through the generic pointer the compiler must
+    // assume the shared-memory stores below may alias them
+    const int dim = p.dim, t = p.t;
+    const float *__restrict__ queries = p.queries;
+    const float *__restrict__ centroids = p.centroids;
+    const int32_t *__restrict__ sub_off = p.sub_off;
+    const int32_t *__restrict__ sub_size = p.sub_size;
+    const int n4 = (int)(p.bloom_stride >> 2);
+    const uint32_t mp1 = p.medoid_p1, mp2 = p.medoid_p2;
+    for (int i = tid; i < dim; i += NT) s_q[i] = __ldg(queries + qid * dim + i);
+    for (int i = tid; i < t; i += NT) s_vis[i] = 0;
+    {   // the filter starts empty (whole-line stores)
+        uint4 *b4 = reinterpret_cast<uint4 *>(bits);
+        for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
+    }
+    __syncthreads();
+    // kernel 1 for this query into shared memory (pq.py:284-296); the
+    // centroid loads (L2) of 8 entries per thread are in flight together
+#pragma unroll 8
+    for (int idx = tid; idx < M * 256; idx += NT) {
+        const int s = idx >> 8, c = idx & 255;
+        float e;
+        if constexpr (SUB == 4) {
+            e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
+                             __ldg(reinterpret_cast<const float4 *>(centroids) + s * 256 + c));
+        } else if constexpr (SUB == 2) {
+            e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
+                             __ldg(reinterpret_cast<const float2 *>(centroids) + s * 256 + c));
+        } else {
+            const int off = __ldg(sub_off + s), sz = __ldg(sub_size + s);
+            const float *src = centroids + (int64_t)off * 256 + c * sz;
+            float dd = __fsub_rn(s_q[off], __ldg(src));
+            float a = __fmul_rn(dd, dd);
+            for (int q = 1; q < sz; ++q) {
+                dd = __fsub_rn(s_q[off + q], __ldg(src + q));
+                a = __fadd_rn(a, __fmul_rn(dd, dd));
+            }
+            e = a;
+        }
+        s_tab[idx] = e;
+    }
+    if (tid == 0) {  // the medoid in the filter (engine.py:127-128)
+        const uint32_t w1 = mp1 >> 5, w2 = mp2 >> 5;
+        const uint32_t b1 = 1u << (mp1 & 31), b2 = 1u << (mp2 & 31);
+        if (w1 == w2) {
+            __stcg(bits + w1, b1 | b2);
+        } else {
+            __stcg(bits + w1, b1);
+            __stcg(bits + w2, b2);
+        }
+    }
+    __syncthreads();
+}
+
+// Per-query epilogue (engine.py:244-269): re-rank of the visit
+// log (kernel 5) with the rows staged through the dead table and the keys
+// kept in shared memory for the top-k, or the worklist's first k without
+// re-rank.  Returns the re-ranked candidates (thread 0), 0 if the log
+// overflowed (the host re-runs the query).
+template <int MV>
+__device__ __forceinline__ int split_epilogue(const SearchParams &p, int64_t qid, int iters, int cnt,
+                                           const int32_t *log, const float *s_q, const uint64_t *s_wl,
+                                           float *s_tab, uint64_t *rr) {
+    constexpr int M = 16 * MV;
+    const int tid = threadIdx.x;
+    int32_t *oid = p.out_ids + qid * p.k;
+    float *odist = p.out_dists + qid * p.k;
+    if (tid == 0) {
+        p.out_iters[qid] = iters;
+        p.out_wall_ns[qid] = globaltimer_ns() - p.counters[kCtrT0];
+    }
+    if (!p.rerank) {
+        if (p.log_cap < iters && tid == 0) {
+            const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+            p.overflow_list[at] = (int32_t)qid;
+        }
+        for (int q = tid; q < p.k; q += 128) {
+            if (q < cnt) {
+                oid[q] = (int32_t)key_id(s_wl[q]);
+                odist[q] = key_dist(s_wl[q]);
+            } else {
+                oid[q] = -1;
+                odist[q] = __int_as_float(0x7f800000);
+            }
+        }
+        if (tid == 0) p.out_short[qid] = cnt < p.k;
+        return 0;
+    }
+    if (iters > p.log_cap) {  // visit log truncated: the host re-runs this query
+        if (tid == 0) {
+            const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
+            p.overflow_list[at] = (int32_t)qid;
+        }
+        return 0;
+    }
+    // kernel 5: exact distances of the visit log, then top-k (warp 0)
+    __threadfence_block();
+    __syncthreads();
+    const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
+    const int tab_b = M * 256 * 4, kb = (8 * iters + 15) & ~15;
+    if (rowb % 16 == 0 && kb <= tab_b / 2 && rowb <= tab_b - kb) {
+        // the table is dead until the next query: stage rows in its place and
+        // keep the keys at its end, so the top-k reads shared memory
+        uint64_t *s_rr = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(s_tab) + tab_b - kb);
+        rerank_staged<128>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), tab_b - kb, s_rr);
+        if (tid < 32) {
+            warp_topk_write_smem(s_rr, iters, p.k, oid, odist);
+            if (tid == 0) p.out_short[qid] = iters < p.k;
+        }
+        return tid == 0 ? iters : 0;
+    }
+    for (int i = tid; i < iters; i += 128) {
+        const uint32_t node = (uint32_t)__ldcg(log + i);
+        rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
+    }
+    __threadfence_block();
+    __syncthreads();
+    if (tid < 32) {
+        warp_topk_write(rr, iters, p.k, oid, odist);
+        if (tid == 0) p.out_short[qid] = iters < p.k;
+    }
+    return tid == 0 ? iters : 0;
+}
+
+template <int PL, int SUB, int MV>
+__global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(const __grid_constant__ SearchParams p) {
     constexpr int M = 16 * MV;
     constexpr int RPAD = 64 * PL;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -497,50 +639,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
         if (qi >= p.nq) break;
         const int64_t qid = p.query_map ? (int64_t)p.query_map[qi] : qi;
 
-        for (int i = tid; i < p.dim; i += NT) s_q[i] = __ldg(p.queries + qid * p.dim + i);
-        for (int i = tid; i < t; i += NT) s_vis[i] = 0;
-        {   // the filter starts empty (whole-line stores)
-            uint4 *b4 = reinterpret_cast<uint4 *>(bits);
-            const int n4 = (int)(p.bloom_stride >> 2);
-            for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
-        }
-        __syncthreads();
-        // kernel 1 for this query into shared memory (pq.py:284-296); the
-        // centroid loads (L2) of 8 entries per thread are in flight together
-#pragma unroll 8
-        for (int idx = tid; idx < M * 256; idx += NT) {
-            const int s = idx >> 8, c = idx & 255;
-            float e;
-            if constexpr (SUB == 4) {
-                e = table_entry4(*reinterpret_cast<const float4 *>(s_q + s * 4),
-                                 __ldg(reinterpret_cast<const float4 *>(p.centroids) + s * 256 + c));
-            } else if constexpr (SUB == 2) {
-                e = table_entry2(*reinterpret_cast<const float2 *>(s_q + s * 2),
-                                 __ldg(reinterpret_cast<const float2 *>(p.centroids) + s * 256 + c));
-            } else {
-                const int off = __ldg(p.sub_off + s), sz = __ldg(p.sub_size + s);
-                const float *src = p.centroids + (int64_t)off * 256 + c * sz;
-                float dd = __fsub_rn(s_q[off], __ldg(src));
-                float a = __fmul_rn(dd, dd);
-                for (int q = 1; q < sz; ++q) {
-                    dd = __fsub_rn(s_q[off + q], __ldg(src + q));
-                    a = __fadd_rn(a, __fmul_rn(dd, dd));
-                }
-                e = a;
-            }
-            s_tab[idx] = e;
-        }
-        if (tid == 0) {  // the medoid in the filter (engine.py:127-128)
-            const uint32_t w1 = p.medoid_p1 >> 5, w2 = p.medoid_p2 >> 5;
-            const uint32_t b1 = 1u << (p.medoid_p1 & 31), b2 = 1u << (p.medoid_p2 & 31);
-            if (w1 == w2) {
-                __stcg(bits + w1, b1 | b2);
-            } else {
-                __stcg(bits + w1, b1);
-                __stcg(bits + w2, b2);
-            }
-        }
-        __syncthreads();
+        split_prologue<SUB, MV>(p, qid, s_q, s_vis, s_tab, bits);
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
         if (tid == 64) {
             // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125), expanded at once
@@ -555,28 +654,35 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
             s_m->cnt[0] = 1;
         }
-        if (roww) split_row<PL, MV>(p, (uint32_t)p.medoid, tid, s_tab, bits, s_key, s_m, 0, s_stage, s_tf, kSentinel);
         if (p.profile && tid == 0) {
             const long long now_ = clock64();
             s_m->ph[7] += (unsigned long long)(now_ - c_q);
         }
         __syncthreads();
 
-        int iters = 1, par = 0;
+        // hop 0 is the medoid's row (row warps only, written at parity 0);
+        // hop h >= 1 expands the eager winner chosen at its barrier.  One
+        // call site per role keeps the hop loop's code compact.
+        int iters = 0, par = 1;
         for (;;) {
-            // ---- the hop barrier: eager winner and convergence (engine.py:201-217)
-            const uint64_t rmin = min(s_m->rmin[par][0], s_m->rmin[par][1]);
-            const uint64_t head = s_m->head[par];
-            const uint64_t thr = s_m->thr[par];
-            const uint64_t winner = rmin < head ? rmin : head;
-            st_probes += s_m->rdeg[par];
-            st_fresh += s_m->rfresh[par][0] + s_m->rfresh[par][1];
-            if (head == kSentinel && !(rmin < thr)) break;  // merged worklist all visited
+            uint64_t winner, head = kSentinel, thr = kSentinel;
+            if (iters == 0) {
+                winner = (uint64_t)(uint32_t)p.medoid;
+            } else {
+                // ---- the hop barrier: eager winner and convergence (engine.py:201-217)
+                const uint64_t rmin = min(s_m->rmin[par][0], s_m->rmin[par][1]);
+                head = s_m->head[par];
+                thr = s_m->thr[par];
+                winner = rmin < head ? rmin : head;
+                st_probes += s_m->rdeg[par];
+                st_fresh += s_m->rfresh[par][0] + s_m->rfresh[par][1];
+                if (head == kSentinel && !(rmin < thr)) break;  // merged worklist all visited
+            }
             const long long c0 = prof ? clock64() : 0;
             if (roww) {
                 split_row<PL, MV>(p, key_id(winner), tid, s_tab, bits, s_key + (par ^ 1) * RPAD, s_m, par ^ 1,
-                                  s_stage, s_tf, thr);
-            } else {
+                                  s_stage, s_tf);
+            } else if (iters > 0) {
                 split_list<PL>(p, tid - 64, s_wl, s_vis, s_key + par * RPAD, s_nk, s_sk, s_c, s_spos, s_m, par ^ 1,
                                winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters);
             }
@@ -594,74 +700,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
         c_q = p.profile ? clock64() : 0;
 
         // ---- outputs (engine.py:244-269)
-        const int cnt = s_m->cnt[par];
-        int32_t *oid = p.out_ids + qid * p.k;
-        float *odist = p.out_dists + qid * p.k;
-        if (tid == 0) {
-            p.out_iters[qid] = iters;
-            p.out_wall_ns[qid] = globaltimer_ns() - p.counters[kCtrT0];
-        }
-        if (p.rerank) {
-            if (iters > p.log_cap) {  // visit log truncated: the host re-runs this query
-                if (tid == 0) {
-                    const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
-                    p.overflow_list[at] = (int32_t)qid;
-                }
-                __syncthreads();
-                continue;
-            }
-            // kernel 5: exact distances of the visit log, then top-k (warp 0)
-            __threadfence_block();
-            __syncthreads();
-            const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
-            const int tab_b = M * 256 * 4, kb = (8 * iters + 15) & ~15;
-            if (rowb % 16 == 0 && kb <= tab_b / 2 && rowb <= tab_b - kb) {
-                // the table is dead until the next query: stage rows in its
-                // place and keep the keys at its end, so the top-k reads
-                // shared memory
-                uint64_t *s_rr = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(s_tab) + tab_b - kb);
-                rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), tab_b - kb, s_rr);
-                st_rr += (tid == 0) ? iters : 0;
-                if (tid < 32) {
-                    warp_topk_write_smem(s_rr, iters, p.k, oid, odist);
-                    if (tid == 0) p.out_short[qid] = iters < p.k;
-                }
-                __syncthreads();
-                if (p.profile && tid == 0) s_m->ph[7] += (unsigned long long)(clock64() - c_q);
-                continue;
-            }
-            if (rowb % 16 == 0 && rowb <= M * 256 * 4) {
-                // the table is dead until the next query: stage rows in its place
-                rerank_staged<NT>(p, log, iters, s_q, reinterpret_cast<uint8_t *>(s_tab), M * 256 * 4, rr);
-            } else {
-                for (int i = tid; i < iters; i += NT) {
-                    const uint32_t node = (uint32_t)__ldcg(log + i);
-                    rr[i] = pack_key(exact_sq_dist(p.vectors, p.vec_dtype, p.dim, node, s_q), node);
-                }
-            }
-            st_rr += (tid == 0) ? iters : 0;
-            __threadfence_block();
-            __syncthreads();
-            if (tid < 32) {
-                warp_topk_write(rr, iters, p.k, oid, odist);
-                if (tid == 0) p.out_short[qid] = iters < p.k;
-            }
-        } else {
-            if (p.log_cap < iters && tid == 0) {
-                const unsigned long long at = atomicAdd(p.counters + kCtrOverflow, 1ull);
-                p.overflow_list[at] = (int32_t)qid;
-            }
-            for (int q = tid; q < p.k; q += NT) {
-                if (q < cnt) {
-                    oid[q] = (int32_t)key_id(s_wl[q]);
-                    odist[q] = key_dist(s_wl[q]);
-                } else {
-                    oid[q] = -1;
-                    odist[q] = __int_as_float(0x7f800000);
-                }
-            }
-            if (tid == 0) p.out_short[qid] = cnt < p.k;
-        }
+        st_rr += split_epilogue<MV>(p, qid, iters, s_m->cnt[par], log, s_q, s_wl, s_tab, rr);
         __syncthreads();
         if (p.profile && tid == 0) s_m->ph[7] += (unsigned long long)(clock64() - c_q);
     }

@@ -390,22 +390,20 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch", "split-noexit"])
+@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch"])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
     """CTA kernels with small Bloom filters: most rows share slots, so the
     warp replay from pre-state bits (replay_row_warp) runs constantly.
     cta: search_cta_kernel (filter cleared per query; -summary: smem bitmap of
     written words instead); split: search_split_kernel (with and without the
-    head-row / re-rank-vector L2 prefetches and the ADC early exit)."""
+    head-row L2 prefetch)."""
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     if flow.startswith("cta"):
         s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
     else:
-        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1,
-                     vec_prefetch=0 if flow == "split-noprefetch" else 1,
-                     adc_early_exit=0 if flow == "split-noexit" else 1)
+        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1)
     want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
     assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8)
@@ -516,7 +514,7 @@ def test_pipelined_cta_kernel_matches_oracle(seed, n, d, R, m, t, dtype):
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     want = _oracle_search(q, graph, cb, codes, base, t)
     for kernel, kid in (("auto", 8), ("cta", 2), ("split", 8)):
-        res = s.set_kernel(kernel, vec_prefetch=int(kernel == "split")).search(q)
+        res = s.set_kernel(kernel).search(q)
         assert s.last_stats()["kernel"] == kid
         _same_as_oracle(res, want)
 
