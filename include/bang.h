@@ -59,7 +59,7 @@ typedef int32_t bang_status;
 
 /* Search kernels (bang_options.kernel; bang_search_stats.kernel reports the
  * one that ran as 0 search_kernel, 2 search_cta_kernel, 8 search_split_kernel). */
-#define BANG_KERNEL_AUTO 0  /* split for t <= 256 (m = 32/48), else cta; warp otherwise            */
+#define BANG_KERNEL_AUTO 0  /* split for an HBM graph and t <= 256 (m = 32/48), else cta; warp otherwise */
 #define BANG_KERNEL_WARP 1  /* search_kernel: one warp per query, every ADC data flow               */
 #define BANG_KERNEL_CTA 2   /* search_cta_kernel: one CTA per query, per-query smem table          */
 #define BANG_KERNEL_SPLIT 4 /* search_split_kernel: row warps build the next hop's keys while list
@@ -76,7 +76,10 @@ typedef struct bang_options {
     int32_t l2_persist;   /* 1: the Bloom filters get an L2-persisting access window      */
     int32_t profile;      /* with BANG_PROFILE_PHASES: 2 = search_split_kernel's row-warp
                              stages, 3 = its list-warp stages                            */
-    int32_t reserved[11];
+    int32_t slot_cache;   /* 1: the Bloom slots of every adjacency entry are computed once per
+                             (index, bloom_entries) into HBM (n x R x 8 B, only if that is at
+                             most 1/4 of the free memory) and read with the row (split kernel) */
+    int32_t reserved[10];
 } bang_options;
 
 typedef struct bang_index bang_index;

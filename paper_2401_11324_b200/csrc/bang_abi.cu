@@ -133,6 +133,10 @@ struct bang_index {
     DevBuf<int64_t> offs;
     DevBuf<int32_t> csr;
     DevBuf<uint8_t> skip;
+    // Bloom slots of every adjacency entry for one bloom_entries value
+    // (bang_options.slot_cache): slot_rows[i*R + j] = (p1, p2) of adj[i][j]
+    DevBuf<uint2> slot_rows;
+    int64_t slot_z = 0;
     // last search
     bang_search_stats stats{};
     int64_t last_nq = 0, last_log_cap = 0, log_cap_override = 0;
@@ -199,7 +203,11 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
     const bool split_ok = t <= 256;
     if (o.kernel == BANG_KERNEL_SPLIT && !split_ok)
         return fail(BANG_E_PARAM, "search_split_kernel needs t <= 256 (t=%d)", t);
-    if (!forced_generic && mv > 0 && split_ok && (o.kernel == BANG_KERNEL_SPLIT || o.kernel == BANG_KERNEL_AUTO)) {
+    // AUTO: split for HBM graphs; host-mapped rows go to search_cta_kernel,
+    // whose warp-0 16-byte row copies make fewer PCIe read requests (C4r:
+    // 259 K vs 224 K QPS, profiles/r02/bench_C4r_*.json)
+    const bool split_auto = o.kernel == BANG_KERNEL_AUTO && !ix->host_graph;
+    if (!forced_generic && mv > 0 && split_ok && (o.kernel == BANG_KERNEL_SPLIT || split_auto)) {
         const int spl = rpad <= 64 ? 1 : 2;
         const int srpad = 64 * spl;
         pl.variant = kAdcSmemTable;
@@ -377,6 +385,46 @@ void persist_release(bang_index *ix) {
     }
 }
 
+// Bloom slots of every adjacency entry (bloom.py:26-42 with z = g.z): the
+// search kernel then reads a row's slots with its ids instead of hashing.
+__global__ void slot_rows_kernel(const int32_t *__restrict__ adj, int64_t n_entries, BloomGeom g,
+                                 uint2 *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_entries;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = adj[i];
+        out[i] = v >= 0 ? make_uint2(mod_z(fnv1a((uint32_t)v, kFnvOffset), g), mod_z(fnv1a((uint32_t)v, kFnvOffsetH2), g))
+                        : make_uint2(0u, 0u);
+    }
+}
+
+// The slot cache for z, built on first use (n x R x 8 bytes of HBM; skipped
+// when that exceeds a quarter of the free memory).  Returns whether it is
+// usable.
+bool ensure_slot_cache(bang_index *ix, int64_t z, cudaStream_t st) {
+    if (ix->host_graph || !ix->opts.slot_cache) return false;
+    if (ix->slot_z == z && ix->slot_rows.p) return true;
+    const size_t entries = (size_t)ix->n * ix->R;
+    size_t free_b = 0, total_b = 0;
+    if (!ix->slot_rows.p || ix->slot_rows.n < entries) {
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (entries * sizeof(uint2) > free_b / 4) return false;
+        if (ix->slot_rows.reserve(entries)) {
+            ix->slot_z = 0;
+            return false;
+        }
+    }
+    BloomGeom g;
+    g.z = (uint64_t)z;
+    g.magic = ~0ull / (uint64_t)z;
+    slot_rows_kernel<<<ix->sm_count * 8, 256, 0, st>>>(ix->adj, (int64_t)entries, g, ix->slot_rows.p);
+    if (cudaGetLastError() != cudaSuccess) return false;
+    ix->slot_z = z;
+    return true;
+}
+
 // Enqueue one search pass.  Outputs are indexed by query id; log rows by
 // pass index when qmap != nullptr.
 bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, int64_t nq_pass,
@@ -448,6 +496,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
+    p.slot_rows = pl.kernel == kKSplit && ensure_slot_cache(ix, z, st) ? ix->slot_rows.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -782,6 +831,7 @@ void bang_index_destroy(bang_index *ix) {
         cudaFree(ix->vectors);
     }
     ix->q.release();
+    ix->slot_rows.release();
     ix->table.release();
     ix->ids.release();
     ix->iters.release();
@@ -984,6 +1034,7 @@ void bang_options_default(bang_options *o) {
     *o = bang_options{};
     o->kernel = BANG_KERNEL_AUTO;
     o->row_prefetch = 1;
+    o->slot_cache = 1;
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;
