@@ -76,10 +76,7 @@ typedef struct bang_options {
     int32_t l2_persist;   /* 1: the Bloom filters get an L2-persisting access window      */
     int32_t profile;      /* with BANG_PROFILE_PHASES: 2 = search_split_kernel's row-warp
                              stages, 3 = its list-warp stages                            */
-    int32_t slot_cache;   /* 1: the Bloom slots of every adjacency entry are computed once per
-                             (index, bloom_entries) into HBM (n x R x 8 B, only if that is at
-                             most 1/4 of the free memory) and read with the row (split kernel) */
-    int32_t reserved[10];
+    int32_t reserved[11];
 } bang_options;
 
 typedef struct bang_index bang_index;

@@ -133,10 +133,6 @@ struct bang_index {
     DevBuf<int64_t> offs;
     DevBuf<int32_t> csr;
     DevBuf<uint8_t> skip;
-    // Bloom slots of every adjacency entry for one bloom_entries value
-    // (bang_options.slot_cache): slot_rows[i*R + j] = (p1, p2) of adj[i][j]
-    DevBuf<uint2> slot_rows;
-    int64_t slot_z = 0;
     // last search
     bang_search_stats stats{};
     int64_t last_nq = 0, last_log_cap = 0, log_cap_override = 0;
@@ -385,46 +381,6 @@ void persist_release(bang_index *ix) {
     }
 }
 
-// Bloom slots of every adjacency entry (bloom.py:26-42 with z = g.z): the
-// search kernel then reads a row's slots with its ids instead of hashing.
-__global__ void slot_rows_kernel(const int32_t *__restrict__ adj, int64_t n_entries, BloomGeom g,
-                                 uint2 *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_entries;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = adj[i];
-        out[i] = v >= 0 ? make_uint2(mod_z(fnv1a((uint32_t)v, kFnvOffset), g), mod_z(fnv1a((uint32_t)v, kFnvOffsetH2), g))
-                        : make_uint2(0u, 0u);
-    }
-}
-
-// The slot cache for z, built on first use (n x R x 8 bytes of HBM; skipped
-// when that exceeds a quarter of the free memory).  Returns whether it is
-// usable.
-bool ensure_slot_cache(bang_index *ix, int64_t z, cudaStream_t st) {
-    if (ix->host_graph || !ix->opts.slot_cache) return false;
-    if (ix->slot_z == z && ix->slot_rows.p) return true;
-    const size_t entries = (size_t)ix->n * ix->R;
-    size_t free_b = 0, total_b = 0;
-    if (!ix->slot_rows.p || ix->slot_rows.n < entries) {
-        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        if (entries * sizeof(uint2) > free_b / 4) return false;
-        if (ix->slot_rows.reserve(entries)) {
-            ix->slot_z = 0;
-            return false;
-        }
-    }
-    BloomGeom g;
-    g.z = (uint64_t)z;
-    g.magic = ~0ull / (uint64_t)z;
-    slot_rows_kernel<<<ix->sm_count * 8, 256, 0, st>>>(ix->adj, (int64_t)entries, g, ix->slot_rows.p);
-    if (cudaGetLastError() != cudaSuccess) return false;
-    ix->slot_z = z;
-    return true;
-}
-
 // Enqueue one search pass.  Outputs are indexed by query id; log rows by
 // pass index when qmap != nullptr.
 bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, int64_t nq_pass,
@@ -496,7 +452,6 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
-    p.slot_rows = pl.kernel == kKSplit && ensure_slot_cache(ix, z, st) ? ix->slot_rows.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -831,7 +786,6 @@ void bang_index_destroy(bang_index *ix) {
         cudaFree(ix->vectors);
     }
     ix->q.release();
-    ix->slot_rows.release();
     ix->table.release();
     ix->ids.release();
     ix->iters.release();
@@ -1034,7 +988,6 @@ void bang_options_default(bang_options *o) {
     *o = bang_options{};
     o->kernel = BANG_KERNEL_AUTO;
     o->row_prefetch = 1;
-    o->slot_cache = 1;
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;

@@ -85,9 +85,6 @@ struct SearchParams {
     int32_t row_prefetch;
     // graph + vectors in pinned, mapped host memory (mode="pipelined")
     int32_t host_graph;
-    // search_split_kernel: Bloom slots of every adjacency entry for this
-    // launch's z (n x R, row-major like adj), or nullptr: hash on the fly
-    const uint2 *slot_rows;
     // search_split_kernel: the row keys (double-buffered) at off_code
     int32_t off_code;
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:

@@ -40,7 +40,6 @@ struct SplitMisc {
     int cnt[2];                  // [parity]: worklist entries
     int wsurv[2];                // list warps: survivors per list warp
     int opos;                    // list warps: old position of okey (cnt if none)
-    int qiters, qcnt;            // the query's expansions and final worklist count
     int coll;                    // row warps: in-row slot sharing seen
     long long qi;
     unsigned long long ph[8];  // phase profiler
@@ -174,31 +173,12 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     // and the row's sets do not wait for HBM (issuing the copies first was
     // measured 7% slower: the Bloom words are the longer chain).
     uint32_t p1[PL], p2[PL], wd1[PL], wd2[PL];
-    if (p.slot_rows) {
-        // the slots were computed once per (index, z): read with the row
-        const uint2 *srow = p.slot_rows + (int64_t)w * p.R;
-#pragma unroll
-        for (int r = 0; r < PL; ++r) {
-            p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
-            if (rt + 64 * r < p.R) {
-                const uint2 v = __ldg(srow + rt + 64 * r);
-                p1[r] = v.x;
-                p2[r] = v.y;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int r = 0; r < PL; ++r) {
-            p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
-            if (rt + 64 * r < deg) {
-                p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
-                p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
-            }
-        }
-    }
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
+        p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
         if (rt + 64 * r < deg) {
+            p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
+            p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
             wd1[r] = __ldcg(bits + (p1[r] >> 5));
             wd2[r] = __ldcg(bits + (p2[r] >> 5));
         }
@@ -321,20 +301,12 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #undef SPLIT_STAMP
 }
 
-__device__ __forceinline__ void split_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// List warps, one hop: merge the survivors of s_key (keys < thr) into the
-// worklist (kernels.py:68-87: rank of each entry in the other list, old
-// entries first on ties -- keys are unique), mark the winner visited and log
-// it (engine.py:167-178).  The row warps need only the next head, threshold
-// and count, so those are published first (the "fast part", then
-// bar.arrive on the row barrier) and the scatter of the merge follows while
-// the row warps already work on the next hop.  lt = thread index among the
-// 64 list threads; nxt = parity of the next hop.  s_c (t int16): survivors
-// below each old entry; s_spos (RPAD int16): merged position of each sorted
-// survivor; s_m->hpos[nxt] (list-private): the next head's merged position.
+// List warps: merge the survivors of s_key (keys < thr) into the worklist
+// (kernels.py:68-87: rank of each entry in the other list, old entries first
+// on ties -- keys are unique), mark the winner visited and log it, publish
+// the next head / threshold / count at parity `nxt`.  lt = thread index
+// among the 64 list threads.  s_c (t int16): survivors below each old entry;
+// s_spos (RPAD int16): final position of each sorted survivor.
 template <int PL>
 __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64_t *s_wl, uint8_t *s_vis,
                                            const uint64_t *s_key, uint64_t *s_nk, uint64_t *s_sk, int16_t *s_c,
@@ -391,38 +363,8 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     }
     split_bar(4, NC);
     SPLIT_STAMP(1, 0)
-    const int ncnt = min(t, cnt + n);
-    const int rs = won_head ? 0 : 1;  // best survivor other than the winner
-    // ---- fast part (thread 0): the next threshold = the merged entry of
-    // rank t-1 (merge path over the two sorted lists), the next head = the
-    // smaller of the next old unvisited entry and the best survivor other
-    // than the winner (none if it is truncated), the next count
-    if (lt == 0) {
-        uint64_t nthr = kSentinel;
-        if (cnt + n >= t) {
-            // i = entries taken from the old list among the first t merged
-            int lo = max(0, t - n), hi = min(cnt, t);
-            while (lo < hi) {
-                const int i = (lo + hi) >> 1;
-                if (s_wl[i] < s_sk[t - i - 1]) lo = i + 1;  // too few old entries
-                else hi = i;
-            }
-            const uint64_t a = lo > 0 ? s_wl[lo - 1] : 0ull, b = t - lo > 0 ? s_sk[t - lo - 1] : 0ull;
-            nthr = a > b ? a : b;
-        }
-        uint64_t hk = s_m->okey;
-        if (rs < n && s_sk[rs] < hk) hk = s_sk[rs];
-        if (hk > nthr) hk = kSentinel;  // truncated (nthr is SENTINEL unless the list is full)
-        s_m->head[nxt] = hk;
-        s_m->thr[nxt] = nthr;
-        s_m->cnt[nxt] = ncnt;
-        // the head may be the next winner: its row to L2
-        if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
-    }
-    split_arrive(2, 128);  // the row warps may choose the next winner
-    SPLIT_STAMP(2, 0)
-    // ---- slow part, kernel 4b: each old entry's count of smaller survivors
-    // (the chunks' binary searches interleaved step by step)
+    // ---- kernel 4b: each old entry's count of smaller survivors (the
+    // chunks' binary searches interleaved step by step)
     const int nch = (cnt + NC - 1) / NC;
     uint64_t mv[MAXCH];
     uint8_t mvv[MAXCH];
@@ -448,6 +390,7 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         for (int c = 0; c < MAXCH; ++c)
             if (c < nch && c * NC + lt < cnt) s_c[c * NC + lt] = (int16_t)mc[c];
     }
+    SPLIT_STAMP(2, mc[0])
     split_bar(4, NC);  // all reads of the old worklist precede the writes
     // ---- merge + truncate to t (engine.py:210-215): old entry i goes to
     // i + c_i; survivors c_{i-1} .. c_i - 1 land just before it, the rest
@@ -481,25 +424,42 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
             }
         }
     }
+    const int ncnt = min(t, cnt + n);
     split_bar(4, NC);  // the merged worklist is complete
     SPLIT_STAMP(3, 0)
-    // ---- expand the winner (engine.py:167-178) at its merged position and
-    // record the next head's merged position
+    // ---- expand the winner (engine.py:167-178); the next head is the
+    // smaller of the next old unvisited entry and the best survivor other
+    // than the winner, at its merged position (none if truncated)
     if (lt == 0) {
         // loads first (the stores below may alias them for the compiler)
         const int op = s_m->opos;
-        const uint64_t okey = s_m->okey, hk = s_m->head[nxt];
+        uint64_t hk = s_m->okey;
+        const int rs = won_head ? 0 : 1;  // best survivor other than the winner
         const int c_h = n > 0 && won_head ? s_c[hpos] : 0;
         const int c_o = n > 0 && op < cnt ? s_c[op] : 0;
         const int sp0 = n > 0 ? s_spos[0] : 0;
+        const uint64_t skr = rs < n ? s_sk[rs] : kSentinel;
         const int spr = rs < n ? s_spos[rs] : t;
+        const uint64_t last = s_wl[t - 1];
         const int wpos = won_head ? hpos + c_h : sp0;
         if (p.debug && (wpos >= t || s_wl[wpos] != winner)) atomicAdd(p.counters + kCtrDebugFail, 1ull);
-        const int hp = hk == kSentinel ? ncnt : (hk == okey ? op + c_o : spr);
-        if (p.debug && hk != kSentinel && (hp >= ncnt || s_wl[hp] != hk)) atomicAdd(p.counters + kCtrDebugFail, 1ull);
+        int hp = op < cnt ? op + c_o : t;
+        if (skr < hk) {
+            hk = skr;
+            hp = spr;
+        }
+        if (hp >= ncnt) {
+            hk = kSentinel;
+            hp = ncnt;
+        }
         if (wpos < t) s_vis[wpos] = 1;
         if (iters < p.log_cap) log[iters] = (int32_t)key_id(winner);
         s_m->hpos[nxt] = hp;
+        s_m->head[nxt] = hk;
+        s_m->thr[nxt] = ncnt == t ? last : kSentinel;
+        s_m->cnt[nxt] = ncnt;
+        // the head may be the next winner: its row to L2
+        if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
     }
     SPLIT_STAMP(4, 0)
 #undef SPLIT_STAMP
@@ -681,87 +641,66 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
 
         split_prologue<SUB, MV>(p, qid, s_q, s_vis, s_tab, bits);
         int32_t *log = p.visit_log + (p.query_map ? qi : qid) * p.log_cap;
+        if (tid == 64) {
+            // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125), expanded at once
+            const uint8_t *row = p.codes + (int64_t)p.medoid * p.code_stride;
+            float acc = 0.0f;
+            for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
+            s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
+            s_vis[0] = 1;
+            if (p.log_cap > 0) log[0] = p.medoid;
+            s_m->head[0] = kSentinel;
+            s_m->hpos[0] = 1;
+            s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
+            s_m->cnt[0] = 1;
+        }
         if (p.profile && tid == 0) {
             const long long now_ = clock64();
             s_m->ph[7] += (unsigned long long)(now_ - c_q);
         }
-
-        // The roles meet through two named barriers per hop: the row warps
-        // arrive on barrier 1 when the row's keys are out and sync on barrier
-        // 2 for the next head; the list warps sync on barrier 1 for the keys
-        // and arrive on barrier 2 as soon as the next head / threshold are
-        // published (the merge's scatter then overlaps the next row).  Hop h
-        // expands w_h: the row warps produce keys_{h+1} (parity (h+1)&1), the
-        // list warps merge keys_h and publish head_{h+1} (parity (h+1)&1).
-        if (roww) {
-            uint32_t w = (uint32_t)p.medoid;  // hop 0: the medoid's row
-            for (int h = 0;; ) {
-                const long long c0 = prof ? clock64() : 0;
-                split_row<PL, MV>(p, w, tid, s_tab, bits, s_key + ((h + 1) & 1) * RPAD, s_m, (h + 1) & 1, s_stage,
-                                  s_tf);
-                long long c1 = 0;
-                if (prof) {
-                    c1 = clock64();
-                    s_m->ph[0] += (unsigned long long)(c1 - c0);
-                }
-                split_arrive(1, 128);
-                ++h;
-                split_bar(2, 128);
-                const int pr = h & 1;
-                const uint64_t rmin = min(s_m->rmin[pr][0], s_m->rmin[pr][1]);
-                const uint64_t head = s_m->head[pr], thr = s_m->thr[pr];
-                if (prof) s_m->ph[2] += (unsigned long long)(clock_after((int)head) - c1);
-                if (head == kSentinel && !(rmin < thr)) break;  // merged worklist all visited (engine.py:217)
-                w = key_id(rmin < head ? rmin : head);           // eager winner (engine.py:201-205)
-            }
-        } else {
-            const int lt = tid - 64;
-            if (lt == 0) {
-                // worklist = [key(ADC(medoid), medoid)] (engine.py:118-125), expanded at once
-                const uint8_t *row = p.codes + (int64_t)p.medoid * p.code_stride;
-                float acc = 0.0f;
-                for (int s = 0; s < M; ++s) acc = __fadd_rn(acc, s_tab[s * 256 + __ldg(row + s)]);
-                s_wl[0] = pack_key(acc, (uint32_t)p.medoid);
-                s_vis[0] = 1;
-                if (p.log_cap > 0) log[0] = p.medoid;
-                s_m->head[1] = kSentinel;
-                s_m->hpos[1] = 1;
-                s_m->thr[1] = t == 1 ? s_wl[0] : kSentinel;
-                s_m->cnt[1] = 1;
-            }
-            split_arrive(2, 128);
-            int h = 1;
-            for (;; ++h) {
-                const long long c0 = prof ? clock64() : 0;
-                split_bar(1, 128);
-                const int pr = h & 1;
-                const uint64_t rmin = min(s_m->rmin[pr][0], s_m->rmin[pr][1]);
-                const uint64_t head = s_m->head[pr], thr = s_m->thr[pr];
-                long long c1 = 0;
-                if (prof) {
-                    c1 = clock_after((int)rmin);
-                    s_m->ph[3] += (unsigned long long)(c1 - c0);
-                }
-                st_probes += s_m->rdeg[pr];
-                st_fresh += s_m->rfresh[pr][0] + s_m->rfresh[pr][1];
-                if (head == kSentinel && !(rmin < thr)) break;
-                const uint64_t winner = rmin < head ? rmin : head;
-                split_list<PL>(p, lt, s_wl, s_vis, s_key + pr * RPAD, s_nk, s_sk, s_c, s_spos, s_m, pr ^ 1, winner,
-                               head, thr, s_m->cnt[pr], s_m->hpos[pr], log, h);
-                if (prof) s_m->ph[1] += (unsigned long long)(clock64() - c1);
-            }
-            if (lt == 0) {
-                s_m->qiters = h;
-                s_m->qcnt = s_m->cnt[h & 1];
-            }
-        }
         __syncthreads();
-        const int iters = s_m->qiters;
+
+        // hop 0 is the medoid's row (row warps only, written at parity 0);
+        // hop h >= 1 expands the eager winner chosen at its barrier.  One
+        // call site per role keeps the hop loop's code compact.
+        int iters = 0, par = 1;
+        for (;;) {
+            uint64_t winner, head = kSentinel, thr = kSentinel;
+            if (iters == 0) {
+                winner = (uint64_t)(uint32_t)p.medoid;
+            } else {
+                // ---- the hop barrier: eager winner and convergence (engine.py:201-217)
+                const uint64_t rmin = min(s_m->rmin[par][0], s_m->rmin[par][1]);
+                head = s_m->head[par];
+                thr = s_m->thr[par];
+                winner = rmin < head ? rmin : head;
+                st_probes += s_m->rdeg[par];
+                st_fresh += s_m->rfresh[par][0] + s_m->rfresh[par][1];
+                if (head == kSentinel && !(rmin < thr)) break;  // merged worklist all visited
+            }
+            const long long c0 = prof ? clock64() : 0;
+            if (roww) {
+                split_row<PL, MV>(p, key_id(winner), tid, s_tab, bits, s_key + (par ^ 1) * RPAD, s_m, par ^ 1,
+                                  s_stage, s_tf);
+            } else if (iters > 0) {
+                split_list<PL>(p, tid - 64, s_wl, s_vis, s_key + par * RPAD, s_nk, s_sk, s_c, s_spos, s_m, par ^ 1,
+                               winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters);
+            }
+            long long c1 = 0;
+            if (prof) {
+                c1 = clock64();
+                s_m->ph[tid == 0 ? 0 : 1] += (unsigned long long)(c1 - c0);
+            }
+            ++iters;
+            par ^= 1;
+            __syncthreads();
+            if (prof) s_m->ph[tid == 0 ? 2 : 3] += (unsigned long long)(clock_after(s_m->cnt[par]) - c1);
+        }
         st_iters += iters;
         c_q = p.profile ? clock64() : 0;
 
         // ---- outputs (engine.py:244-269)
-        st_rr += split_epilogue<MV>(p, qid, iters, s_m->qcnt, log, s_q, s_wl, s_tab, rr);
+        st_rr += split_epilogue<MV>(p, qid, iters, s_m->cnt[par], log, s_q, s_wl, s_tab, rr);
         __syncthreads();
         if (p.profile && tid == 0) s_m->ph[7] += (unsigned long long)(clock64() - c_q);
     }
@@ -775,8 +714,6 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
     if (tid == 0) {
         atomicAdd(p.counters + kCtrIterations, st_iters);
         atomicAdd(p.counters + kCtrRerank, st_rr);
-    }
-    if (tid == 64) {  // the list warps read the rows' counts at each hop
         atomicAdd(p.counters + kCtrProbes, st_probes);
         atomicAdd(p.counters + kCtrFresh, st_fresh);
     }

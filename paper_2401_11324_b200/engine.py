@@ -211,8 +211,8 @@ class DeviceIndex:
 
     def set_options(self, kernel: str = "auto", **tuning) -> None:
         """bang_index_set_options: kernel in _lib.KERNEL_CHOICES plus the
-        bang_options tuning fields (row_prefetch, slot_cache, bloom_clear,
-        l2_persist, profile); unnamed fields keep their defaults."""
+        bang_options tuning fields (row_prefetch, bloom_clear, l2_persist,
+        profile); unnamed fields keep their defaults."""
         if kernel not in _lib.KERNEL_CHOICES:
             raise ParameterError(f"unknown kernel {kernel!r}; expected one of {sorted(_lib.KERNEL_CHOICES)}")
         o = _lib.Options()

@@ -390,7 +390,7 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch", "split-noslots"])
+@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch"])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
     """CTA kernels with small Bloom filters: most rows share slots, so the
     warp replay from pre-state bits (replay_row_warp) runs constantly.
@@ -403,8 +403,7 @@ def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, f
     if flow.startswith("cta"):
         s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
     else:
-        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1,
-                     slot_cache=0 if flow == "split-noslots" else 1)
+        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1)
     want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
     assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8)
@@ -571,17 +570,3 @@ def test_stats_counters_are_consistent():
     assert st["probes"] == int(sum(deg[log].sum() for log in res.visit_logs))
     assert st["kernel_ms"] > 0
 
-
-def test_split_slot_cache_follows_bloom_entries():
-    """The per-(index, z) Bloom slot cache is rebuilt when bloom_entries
-    changes between searches on one index (and matches hashing on the fly)."""
-    base, q, graph, cb, codes = _random_case(27, 12_000, 96, 64, 48, 120, np.float32)
-    s = B.GraphSearcher(k=10, t=64, mode="in_memory", debug_checks=True)
-    s.fit(base, graph=graph, codebook=cb, codes=codes)
-    for z in (399_887, 1021, 399_887, 4099):
-        s.bloom_entries = z
-        want = _oracle_search(q, graph, cb, codes, base, 64, z)
-        for cache in (1, 0):
-            res = s.set_kernel("split", slot_cache=cache).search(q)
-            assert s.last_stats()["kernel"] == 8
-            _same_as_oracle(res, want)
