@@ -301,7 +301,8 @@ def main():
         return
 
     from paper_2401_11324_b200 import GraphSearcher, _lib, set_device
-    from paper_2401_11324_b200.tools.bench_data import CONFIGS, EXACT_KNN_LIMIT, THROUGHPUT_CONFIGS, build_artifacts
+    from paper_2401_11324_b200.tools.bench_data import (CONFIGS, EXACT_KNN_LIMIT, HOST_GRAPH_CONFIGS, PARTITIONED,
+                                                        THROUGHPUT_CONFIGS, build_artifacts)
     set_device(local)
     thr_only = args.config in THROUGHPUT_CONFIGS
     nq_cfg = 1_000 if args.config == "C1" else (THROUGHPUT_CONFIGS[args.config] if thr_only
@@ -327,7 +328,8 @@ def main():
     queries = np.ascontiguousarray(art["queries"][lo:hi], np.float32)
     gt = None if thr_only else np.asarray(art["gt_ids"][lo:hi])
     nq = queries.shape[0]
-    mode = "pipelined" if thr_only else "in_memory"  # throughput shapes: graph in pinned host memory
+    # throughput shapes and C4: graph + vectors in pinned host memory
+    mode = "pipelined" if thr_only or args.config in HOST_GRAPH_CONFIGS else "in_memory"
     meta = art["meta"]
     t_fixed = args.t or (meta["t"] if thr_only else 0)
     config = {"workload": args.config, "desc": meta["desc"], "n": meta["n"], "dim": meta["dim"],
@@ -339,6 +341,10 @@ def main():
                         if thr_only else
                         "GPU kNN(2R) + RobustPrune(1.2) + reverse edges (tools/graph_build.py)"
                         if meta["n"] <= EXACT_KNN_LIMIT else
+                        f"partitioned build (tools/graph_build.build_graph_partitioned: {PARTITIONED[args.config]}): "
+                        "per partition IVF kNN(2R) + RobustPrune(1.2) + reverse edges + search-based Vamana "
+                        "passes; merged by RobustPrune over each point's partition lists"
+                        if args.config in PARTITIONED else
                         "GPU IVF kNN(2R) + RobustPrune(1.2) + reverse edges, then search-based Vamana "
                         "passes (t=128, 128, 200) with this search (tools/graph_build.py)"),
               "l2": "flushed between steps (256 MiB memset outside the step events)",

@@ -25,10 +25,28 @@ CONFIGS = {
            "SIFT1M-shape synthetic 1Mx128 uint8, R=64, PQ 32 subspaces, 10K queries, k=10"),
     "C3": (10_000_000, 10_000, 96, "f32", 100_000, 64, 48,
            "DEEP-shape synthetic 10Mx96 fp32, R=64, PQ 48 subspaces, 10K queries, k=10"),
+    # BASELINE.json configs[3] with a real graph: the graph and vectors live
+    # in pinned host memory (mode="pipelined"); the graph is built in
+    # overlapping partitions (PARTITIONED)
+    "C4": (100_000_000, 10_000, 128, "u8", 1_000_000, 64, 32,
+           "SIFT-shape synthetic 100Mx128 uint8, R=64, PQ 32 subspaces, graph + vectors in pinned host memory, "
+           "10K queries, k=10"),
     # reduced-n variants of the same shapes (parity tests, quick checks)
     "C2s": (100_000, 10_000, 128, "u8", 1_000, 64, 32, "C2 shape at n=100K"),
     "C3s": (200_000, 10_000, 96, "f32", 2_000, 64, 48, "C3 shape at n=200K"),
+    "C3p": (10_000_000, 10_000, 96, "f32", 100_000, 64, 48, "C3 built by partitions (builder check)"),
 }
+
+# Configs whose graph is built in overlapping partitions
+# (graph_build.build_graph_partitioned): parts, overlap, search-based passes
+# per partition.  C4's monolithic build would need ~230 GB of HBM (k-NN
+# candidate tables); C3p checks the partitioned build against C3's.
+PARTITIONED = {
+    "C4": dict(parts=16, overlap=2, refine=(128,)),
+    "C3p": dict(parts=4, overlap=2, refine=(128,)),
+}
+# Configs searched with the graph in pinned host memory (BASELINE.json configs[3])
+HOST_GRAPH_CONFIGS = ("C4",)
 
 
 # Throughput-only shapes (BASELINE.json configs[3..4]; "C5:
@@ -185,16 +203,33 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         if os.path.isdir(path) or load_only:
             return _load_cached(path, name, meta, log)
     t0 = time.time()
-    base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed)
+    base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed,
+                                     out_dtype=np.uint8 if dt == "u8" else np.float32)
     if dt == "u8":
-        base, queries = to_u8(base), to_u8(queries).astype(np.float32)
+        queries = queries.astype(np.float32)
     t1 = time.time()
-    graph = build_graph(base, degree_bound=R, seed=seed, log=log)
-    t2 = time.time()
-    cb = train_codebook(base, m=m, iters=15, seed=seed)
-    codes = encode(base, cb)
-    t3 = time.time()
-    if n > EXACT_KNN_LIMIT:
+    if name in PARTITIONED:
+        from .graph_build import build_graph_partitioned
+        cb = train_codebook(base, m=m, iters=15, seed=seed)
+        codes = encode(base, cb)
+        t2 = time.time()
+        cfg = PARTITIONED[name]
+
+        def refine_fn(members, g, t_ref):
+            return refine_with_search(base[members], g, cb, CompressedVectors(codes.codes[members]), R,
+                                      t=t_ref, log=log)
+
+        graph = build_graph_partitioned(base, degree_bound=R, parts=cfg["parts"], overlap=cfg["overlap"],
+                                        refine_fn=refine_fn, refine=cfg["refine"], seed=seed, log=log)
+        t3 = time.time()
+        t2, t3 = t3 - (t2 - t1), t3  # report graph time apart from PQ time
+    else:
+        graph = build_graph(base, degree_bound=R, seed=seed, log=log)
+        t2 = time.time()
+        cb = train_codebook(base, m=m, iters=15, seed=seed)
+        codes = encode(base, cb)
+        t3 = time.time()
+    if n > EXACT_KNN_LIMIT and name not in PARTITIONED:
         # partitioned k-NN graph -> one search-based Vamana pass with the
         # B200 search itself (the reference's builder, graph.py:251-344,
         # inserts by greedy search too)

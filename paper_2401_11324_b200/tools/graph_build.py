@@ -398,3 +398,89 @@ def refine_graph(x, adj, deg, visit_fn, R: int, sigma: float = 1.2, chunk: int =
     if log:
         log(f"[graph_build] refine: search {t_search:.1f}s prune {t_prune:.1f}s reverse {time.time() - t2:.1f}s")
     return new_adj, new_deg
+
+
+def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overlap: int = 2,
+                            sigma: float = 1.2, refine_fn=None, refine=(), seed: int = 0,
+                            merge_chunk: int = 1 << 19, device=None, log=print) -> GraphIndex:
+    """Graph of a base set too large for one build in HBM (C4: 100M x 128 u8).
+
+    DiskANN-style partitioned construction: k-means on a sample gives
+    `parts` centroids; every point joins its `overlap` nearest partitions;
+    each partition gets its own graph (build_graph, then the search-based
+    Vamana passes `refine_fn(members, local_graph, t)` for t in `refine`);
+    a point's neighbour lists from its partitions are merged with one
+    RobustPrune(sigma) over their union (exact distances).  Shared points
+    connect the partitions.  Memory: the base stays in host RAM (u8 or f32)
+    plus one partition and an (n, overlap*R) int32 candidate table."""
+    import time
+    import torch
+    dev = device if device is not None else torch_device()
+    xn = np.asarray(base)
+    n, d = xn.shape
+    R = int(degree_bound)
+    t0 = time.time()
+    rng = np.random.default_rng(seed)
+    samp = np.sort(rng.choice(n, size=min(n, 1 << 20), replace=False))
+    xs = torch.from_numpy(np.ascontiguousarray(xn[samp], dtype=np.float32)).to(dev)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        cent = kmeans(xs, parts, seed=seed)
+        del xs
+        assign = np.empty((n, overlap), np.int32)
+        for lo in range(0, n, 1 << 22):
+            xb = torch.from_numpy(np.ascontiguousarray(xn[lo:lo + (1 << 22)])).to(dev).float()
+            assign[lo:lo + (1 << 22)] = _nearest_centroids(xb, cent, overlap).to(torch.int32).cpu().numpy()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    log(f"[graph_build] partitioned: {parts} parts x {overlap}-way, assignment {time.time() - t0:.1f}s")
+    # members of each partition (stable order), and which of a point's slots it fills
+    flat = assign.ravel()
+    order = np.argsort(flat, kind="stable")
+    bounds = np.searchsorted(flat[order], np.arange(parts + 1))
+    cand = np.full((n, overlap * R), -1, np.int32)
+    for p in range(parts):
+        t1 = time.time()
+        sel = order[bounds[p]:bounds[p + 1]]
+        members, slot = sel // overlap, sel % overlap
+        if members.size < 2:
+            continue
+        g = build_graph(xn[members], degree_bound=R, sigma=sigma, seed=seed, device=dev)
+        for t in refine:
+            g = refine_fn(members, g, t)
+        adj = g.adjacency
+        glob = np.where(adj >= 0, members[np.clip(adj, 0, None)], -1).astype(np.int32)
+        for j in range(overlap):
+            m_ = slot == j
+            cand[members[m_], j * R:(j + 1) * R] = glob[m_]
+        torch.cuda.empty_cache()
+        log(f"[graph_build] partition {p + 1}/{parts}: {members.size} points, {time.time() - t1:.1f}s")
+    # merge: RobustPrune over the union of each point's partition lists
+    t2 = time.time()
+    x = torch.from_numpy(np.ascontiguousarray(xn)).to(dev)  # native dtype (u8: n*d bytes)
+    adj_out = np.full((n, R), -1, np.int32)
+    deg_out = np.zeros(n, np.int32)
+    for lo in range(0, n, merge_chunk):
+        hi = min(n, lo + merge_chunk)
+        c = torch.from_numpy(cand[lo:hi]).to(dev).long()
+        cs, _ = torch.sort(c, dim=1)
+        dup = torch.zeros_like(cs, dtype=torch.bool)
+        dup[:, 1:] = cs[:, 1:] == cs[:, :-1]
+        c = torch.where(dup, torch.full_like(cs, -1), cs)
+        rows = torch.arange(lo, hi, device=dev)[:, None].expand_as(c)
+        valid = c >= 0
+        dd = torch.full(c.shape, float("inf"), dtype=torch.float32, device=dev)
+        dd[valid] = _pair_sqdist(x, rows[valid], c[valid])
+        c, dd = _sort_rows_by_dist(c, dd)
+        c = torch.where(torch.isinf(dd), torch.full_like(c, -1), c)
+        a, dg = robust_prune(x, c, dd, R, sigma)
+        adj_out[lo:hi] = a.to(torch.int32).cpu().numpy()
+        deg_out[lo:hi] = dg.to(torch.int32).cpu().numpy()
+    medoid = medoid_of(x)
+    del x
+    torch.cuda.empty_cache()
+    adj_out[np.arange(R)[None, :] >= deg_out[:, None]] = -1
+    log(f"[graph_build] partitioned merge {time.time() - t2:.1f}s, total {time.time() - t0:.1f}s "
+        f"(mean degree {deg_out.mean():.1f})")
+    return GraphIndex(adj_out, deg_out, medoid, R, validate=False)
