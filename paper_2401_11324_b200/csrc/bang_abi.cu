@@ -133,6 +133,7 @@ struct bang_index {
     DevBuf<int64_t> offs;
     DevBuf<int32_t> csr;
     DevBuf<uint8_t> skip;
+    unsigned long long *h_ctr = nullptr;  // pinned copy of the counters (one-batch readback)
     // last search
     bang_search_stats stats{};
     int64_t last_nq = 0, last_log_cap = 0, log_cap_override = 0;
@@ -559,9 +560,16 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
 }
 
 // Reads counters after the stream drained; fills stats.
+bang_status collect_stats(bang_index *ix, const unsigned long long *ctr);
+
 bang_status collect(bang_index *ix, unsigned long long *ctr) {
     CU(cudaStreamSynchronize(ix->last_stream));
     CU(cudaMemcpy(ctr, ix->counters.p, sizeof(unsigned long long) * kCtrCount, cudaMemcpyDeviceToHost));
+    return collect_stats(ix, ctr);
+}
+
+// search statistics from counters already on the host (the stream is idle)
+bang_status collect_stats(bang_index *ix, const unsigned long long *ctr) {
     float ms_total = 0.f, ms_table = 0.f;
     CU(cudaEventElapsedTime(&ms_table, ix->ev[0], ix->ev[1]));
     CU(cudaEventElapsedTime(&ms_total, ix->ev[1], ix->ev[2]));
@@ -785,6 +793,7 @@ void bang_index_destroy(bang_index *ix) {
         cudaFree(ix->deg);
         cudaFree(ix->vectors);
     }
+    if (ix->h_ctr) cudaFreeHost(ix->h_ctr);
     ix->q.release();
     ix->table.release();
     ix->ids.release();
@@ -880,6 +889,52 @@ bang_status bang_search(bang_index *ix, const float *queries, int64_t nq, int32_
     if ((s = enqueue_search(ix, ix->q.p, nq, k, t, bloom_entries, flags, ix->ids.p, ix->dists.p, ix->iters.p,
                             ix->shortf.p, st)))
         return s;
+    // One-batch readback when the caller's visit-log buffer is page-locked
+    // and holds the worst case (nq x log capacity): offsets scanned and logs
+    // compacted on the device straight into it, every output and the
+    // counters copied back in one batch, one synchronisation.  An overflowed
+    // visit log falls back to the exact re-run below.
+    {
+        const int64_t cap = ix->last_log_cap;
+        cudaPointerAttributes va{};
+        const bool direct = visit_ids && visit_offsets && visit_cap >= nq * cap &&
+                            cudaPointerGetAttributes(&va, visit_ids) == cudaSuccess &&
+                            (va.type == cudaMemoryTypeHost || va.type == cudaMemoryTypeDevice ||
+                             va.type == cudaMemoryTypeManaged) && va.devicePointer;
+        cudaGetLastError();
+        if (direct) {
+            if (!ix->h_ctr) CU(cudaHostAlloc(reinterpret_cast<void **>(&ix->h_ctr), sizeof(unsigned long long) * kCtrCount,
+                                            cudaHostAllocDefault));
+            if ((s = ix->offs.reserve((size_t)nq + 1))) return s;
+            scan_offsets_kernel<<<1, 1024, 0, st>>>(ix->iters.p, nq, ix->offs.p);
+            compact_logs_kernel<<<(unsigned)ceil_div(nq, 8), 256, 0, st>>>(
+                ix->log.p, cap, nq, nullptr, ix->offs.p, nullptr, static_cast<int32_t *>(va.devicePointer));
+            CU(cudaGetLastError());
+            std::vector<uint64_t> wns(wall ? nq : 0);
+            CU(cudaMemcpyAsync(ix->h_ctr, ix->counters.p, sizeof(unsigned long long) * kCtrCount,
+                               cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(ids, ix->ids.p, sizeof(int32_t) * nq * k, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(dists, ix->dists.p, sizeof(float) * nq * k, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(iterations, ix->iters.p, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, st));
+            CU(cudaMemcpyAsync(visit_offsets, ix->offs.p, sizeof(int64_t) * (nq + 1), cudaMemcpyDeviceToHost, st));
+            if (short_) CU(cudaMemcpyAsync(short_, ix->shortf.p, nq, cudaMemcpyDeviceToHost, st));
+            if (wall) CU(cudaMemcpyAsync(wns.data(), ix->wall.p, sizeof(uint64_t) * nq, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            if ((s = collect_stats(ix, ix->h_ctr))) return s;
+            if (ix->h_ctr[kCtrDebugFail])
+                return fail(BANG_E_STATE, "debug check failed: eager candidate disagrees with the post-merge worklist head");
+            if (!ix->h_ctr[kCtrOverflow]) {
+                if (converged) memset(converged, 1, nq);  // the loop runs every query to convergence
+                if (wall)
+                    for (int64_t i = 0; i < nq; ++i) wall[i] = (double)wns[i] * 1e-9;
+                ix->last_iters.assign(iterations, iterations + nq);
+                ix->last_offsets.assign(visit_offsets, visit_offsets + nq + 1);
+                ix->pending = false;
+                return BANG_OK;
+            }
+            // an overflowed log: redo the readback the general way
+        }
+    }
     unsigned long long ctr[kCtrCount];
     if ((s = collect(ix, ctr))) return s;
     if (ctr[kCtrDebugFail])

@@ -226,8 +226,48 @@ __global__ void compact_logs_kernel(const int32_t *__restrict__ log, int64_t cap
     if (r >= rows) return;
     const int64_t q = map ? map[r] : r;
     if (skip && skip[q]) return;
-    const int64_t lo = off[q], len = off[q + 1] - lo;
+    const int64_t lo = off[q], len = min(off[q + 1] - lo, cap);  // (an overflowed row is re-run)
     for (int64_t i = lane_id(); i < len; i += 32) out[lo + i] = log[r * cap + i];
+}
+
+// CSR offsets of the visit logs from the iteration counts: off[0] = 0,
+// off[i + 1] = off[i] + iters[i]; one CTA, chunk by chunk with a carry.
+__global__ void __launch_bounds__(1024) scan_offsets_kernel(const int32_t *__restrict__ iters, int64_t n,
+                                                            int64_t *__restrict__ off) {
+    __shared__ long long s_w[32];
+    __shared__ long long s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_carry = 0;
+        off[0] = 0;
+    }
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += 1024) {
+        const int64_t i = base + tid;
+        long long v = i < n ? iters[i] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long u = __shfl_up_sync(0xFFFFFFFFu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane == 31) s_w[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            long long w = s_w[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long u = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o) w += u;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        const long long incl = v + (warp > 0 ? s_w[warp - 1] : 0) + s_carry;
+        if (i < n) off[i + 1] = incl;
+        __syncthreads();
+        if (tid == 1023) s_carry = incl;
+        __syncthreads();
+    }
 }
 
 // exact_sq_dists (engine.py:48-51), row-paired, one thread per row.

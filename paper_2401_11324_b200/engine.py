@@ -190,14 +190,19 @@ class DeviceIndex:
         short = np.empty(nq, np.uint8)
         wall = np.empty(nq, np.float64)
         offs = np.empty(nq + 1, np.int64)
+        # a page-locked log buffer for the worst case (nq x the default device
+        # log capacity, bang.h) lets bang_search compact the visit logs
+        # straight into it and read everything back in one batch
+        flat = _dev.pinned_empty(nq * max(1024, 4 * t), np.int32)
         L = _lib.lib()
         st = L.bang_search(self.handle, _lib.ptr(q), nq, k, t, int(bloom_entries), flags, _lib.ptr(ids),
                            _lib.ptr(dists), _lib.ptr(iters), _lib.ptr(conv), _lib.ptr(short),
-                           _lib.ptr(wall), _lib.ptr(offs), None, 0)
+                           _lib.ptr(wall), _lib.ptr(offs), _lib.ptr(flat), flat.size)
+        if st == _lib.BANG_E_CAPACITY:  # longer logs (re-runs): the two-call protocol
+            flat = _dev.pinned_empty(int(offs[-1]), np.int32)
+            st = L.bang_last_visit_logs(self.handle, _lib.ptr(flat), flat.size)
         _lib.check(st, "bang_search")
-        flat = _dev.pinned_empty(int(offs[-1]), np.int32)
-        _lib.check(L.bang_last_visit_logs(self.handle, _lib.ptr(flat), flat.size), "bang_last_visit_logs")
-        return ids, dists, iters, conv.astype(bool), short.astype(bool), wall, offs, flat
+        return ids, dists, iters, conv.astype(bool), short.astype(bool), wall, offs, flat[:int(offs[-1])]
 
     def stats(self) -> dict:
         s = _lib.SearchStats()
