@@ -570,3 +570,23 @@ def test_stats_counters_are_consistent():
     assert st["probes"] == int(sum(deg[log].sum() for log in res.visit_logs))
     assert st["kernel_ms"] > 0
 
+
+
+@pytest.mark.parametrize("cap", [2048, 40])
+def test_public_search_readback_paths(cap):
+    """GraphSearcher.search reads results back in one batch when its
+    page-locked log buffer covers nq x the device log capacity; a larger
+    capacity (cap=2048 > max(1024, 4t)) takes the two-call protocol, a small
+    one (overflow re-runs) the general path.  All equal to the oracle."""
+    from paper_2401_11324_b200 import _lib
+    base, q, graph, cb, codes = _random_case(28, 8_000, 96, 64, 48, 150, np.float32)
+    t = 48
+    s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=399_887, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    want = _oracle_search(q, graph, cb, codes, base, t)
+    res = s.search(q)  # default capacity: the one-batch path
+    _same_as_oracle(res, want)
+    _lib.check(_lib.lib().bang_index_set_log_capacity(s.index_.handle, cap))
+    res = s.search(q)
+    _same_as_oracle(res, want)
+    assert (s.last_stats()["retries"] > 0) == (cap < 60)
