@@ -1150,18 +1150,19 @@ bang_status bang_adc_pairs_device(bang_index *ix, const float *d_queries, int64_
     const int sub = ix->uniform_sub;
     const bool vec = (sub == 4 && mv == 2) || (sub == 2 && mv == 3);
     // table + query (+ per-warp double-buffered code-row stages, vector path)
+    constexpr int NT = BANG_ADC_PAIRS_NT;  // threads per query CTA
     const size_t smem = sizeof(float) * ((size_t)ix->m * 256 + align_up(ix->dim, 4)) +
-                        (vec ? (size_t)8 * 2 * 32 * ix->m : 0);
+                        (vec ? (size_t)(NT / 32) * 2 * 32 * ix->m : 0);
     if (smem > (size_t)ix->max_smem) return fail(BANG_E_PARAM, "table of m=%d does not fit in shared memory", ix->m);
     auto launch = [&](const void *fn) -> bang_status {
         CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int per_sm = 0;
-        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, smem));
         const int64_t grid = std::min<int64_t>(nq, (int64_t)ix->sm_count * std::max(1, per_sm));
         int m = ix->m, dim = ix->dim, cs = ix->code_stride;
         void *args[] = {&ix->centroids, &ix->d_sub_off, &ix->d_sub_size, &m, &dim, &d_queries, &nq,
                         &d_off, &d_ids, &ix->codes, &cs, &d_keys};
-        CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(256), args, smem, st));
+        CU(cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(NT), args, smem, st));
         return BANG_OK;
     };
     if (sub == 4 && mv == 2) return launch(reinterpret_cast<const void *>(&adc_pairs_kernel<4, 2>));

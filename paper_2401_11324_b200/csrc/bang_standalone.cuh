@@ -292,8 +292,11 @@ namespace bang {
 // ids[off[q], off[q+1]).  SUB/MV > 0: uniform subspaces of width SUB and
 // m = 16*MV (vector path); 0: generic.
 // -------------------------------------------------------------------------
+#ifndef BANG_ADC_PAIRS_NT
+#define BANG_ADC_PAIRS_NT 256
+#endif
 template <int SUB, int MV>
-__global__ void __launch_bounds__(256) adc_pairs_kernel(const float *__restrict__ centroids,
+__global__ void __launch_bounds__(BANG_ADC_PAIRS_NT) adc_pairs_kernel(const float *__restrict__ centroids,
                                                         const int32_t *__restrict__ sub_off,
                                                         const int32_t *__restrict__ sub_size, int m,
                                                         int dim, const float *__restrict__ queries,
