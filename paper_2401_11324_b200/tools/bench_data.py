@@ -42,7 +42,7 @@ CONFIGS = {
 # per partition.  C4's monolithic build would need ~230 GB of HBM (k-NN
 # candidate tables); C3p checks the partitioned build against C3's.
 PARTITIONED = {
-    "C4": dict(parts=16, overlap=2, refine=(128,)),
+    "C4": dict(parts=24, overlap=2, refine=(128,)),
     "C3p": dict(parts=4, overlap=2, refine=(128,)),
 }
 # Configs searched with the graph in pinned host memory (BASELINE.json configs[3])

@@ -328,8 +328,13 @@ def build_graph(base, degree_bound: int = 64, build_worklist: int = 200, sigma: 
         ids, d = knn_ivf(x, K, seed=seed)
         medoid = medoid_of(x)
     t1 = time.time()
-    ids, d = _sort_rows_by_dist(ids, d)
-    ids = torch.where(torch.isinf(d), torch.full_like(ids, -1), ids)
+    # row sort in bounded chunks (the full-table argsorts and gathers would
+    # need ~5x the (n, K) int64 table at once)
+    for lo in range(0, n, 1 << 20):
+        si, sd = _sort_rows_by_dist(ids[lo:lo + (1 << 20)], d[lo:lo + (1 << 20)])
+        ids[lo:lo + (1 << 20)] = torch.where(torch.isinf(sd), torch.full_like(si, -1), si)
+        d[lo:lo + (1 << 20)] = sd
+        del si, sd
     adj, deg = robust_prune(x, ids, d, R, sigma)
     del ids, d
     t2 = time.time()
@@ -413,6 +418,7 @@ def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overl
     RobustPrune(sigma) over their union (exact distances).  Shared points
     connect the partitions.  Memory: the base stays in host RAM (u8 or f32)
     plus one partition and an (n, overlap*R) int32 candidate table."""
+    import gc
     import time
     import torch
     dev = device if device is not None else torch_device()
@@ -454,8 +460,15 @@ def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overl
         for j in range(overlap):
             m_ = slot == j
             cand[members[m_], j * R:(j + 1) * R] = glob[m_]
-        torch.cuda.empty_cache()
-        log(f"[graph_build] partition {p + 1}/{parts}: {members.size} points, {time.time() - t1:.1f}s")
+        del g, adj, glob
+        # the partition's device tensors must be gone before the next one
+        # (a reference cycle would otherwise keep ~10 GB per partition alive)
+        gc.collect()
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+        mem = torch.cuda.memory_allocated() / 2**30 if torch.cuda.is_available() else 0.0
+        log(f"[graph_build] partition {p + 1}/{parts}: {members.size} points, {time.time() - t1:.1f}s "
+            f"(device memory in use {mem:.1f} GiB)")
     # merge: RobustPrune over the union of each point's partition lists
     t2 = time.time()
     x = torch.from_numpy(np.ascontiguousarray(xn)).to(dev)  # native dtype (u8: n*d bytes)
