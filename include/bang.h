@@ -76,7 +76,10 @@ typedef struct bang_options {
     int32_t l2_persist;   /* 1: the Bloom filters get an L2-persisting access window      */
     int32_t profile;      /* with BANG_PROFILE_PHASES: 2 = search_split_kernel's row-warp
                              stages, 3 = its list-warp stages                            */
-    int32_t reserved[11];
+    int32_t bloom_direct; /* 1 (split): rows without in-row Bloom slot sharing (a per-(index,
+                             z) bitset, built once) read their pre-state from the fetch-or
+                             itself -- no separate pre-state read and no row barrier     */
+    int32_t reserved[10];
 } bang_options;
 
 typedef struct bang_index bang_index;

@@ -49,8 +49,8 @@ class Options(ctypes.Structure):
     """bang_options (include/bang.h): per-index kernel choice and tuning."""
     _fields_ = [
         ("kernel", ctypes.c_int32), ("row_prefetch", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
-        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 11),
+        ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("bloom_direct", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 10),
     ]
 
     def as_dict(self):

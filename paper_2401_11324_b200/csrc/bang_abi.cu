@@ -145,6 +145,9 @@ struct bang_index {
     std::vector<int32_t> retry_q;
     int64_t retry_cap = 0;
     DevBuf<int32_t> retry_log;
+    // rows with in-row Bloom slot sharing at z = row_share_z (bloom_direct)
+    DevBuf<uint32_t> row_share;
+    int64_t row_share_z = 0;
 };
 
 namespace {
@@ -453,6 +456,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
+    p.row_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -517,6 +521,25 @@ int64_t default_log_cap(const bang_index *ix, int t) {
     return ix->log_cap_override > 0 ? ix->log_cap_override : std::max<int64_t>(1024, 4LL * t);
 }
 
+// The per-(index, z) bitset of rows with in-row Bloom slot sharing
+// (row_share_kernel), built on the first split search at this z.
+bang_status ensure_row_share(bang_index *ix, int64_t z, cudaStream_t st) {
+    if (ix->row_share_z == z) return BANG_OK;
+    const int64_t words = ceil_div(ix->n, 32);
+    bang_status s = ix->row_share.reserve((size_t)words);
+    if (s) return s;
+    CU(cudaMemsetAsync(ix->row_share.p, 0, sizeof(uint32_t) * words, st));
+    BloomGeom g;
+    g.z = (uint64_t)z;
+    g.magic = ~0ull / (uint64_t)z;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(ix->n, kShareWarps), (int64_t)ix->sm_count * 16));
+    row_share_kernel<<<(unsigned)blocks, 32 * kShareWarps, sizeof(uint32_t) * kShareWarps * 2 * ix->R, st>>>(
+        ix->adj, ix->adj_stride, ix->deg, ix->n, ix->R, g, ix->row_share.p);
+    CU(cudaGetLastError());
+    ix->row_share_z = z;
+    return BANG_OK;
+}
+
 bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, int k, int t,
                            int64_t z, int flags, int32_t *d_ids, float *d_dists, int32_t *d_iters,
                            uint8_t *d_short, cudaStream_t st) {
@@ -525,6 +548,7 @@ bang_status enqueue_search(bang_index *ix, const float *d_queries, int64_t nq, i
     if (s) return s;
     const int64_t cap = default_log_cap(ix, t);
     if ((s = ensure_outputs(ix, nq, k, cap))) return s;
+    if (pl.kernel == kKSplit && ix->opts.bloom_direct && (s = ensure_row_share(ix, z, st))) return s;
     CU(cudaEventRecord(ix->ev[0], st));
     record_t0_kernel<<<1, 1, 0, st>>>(ix->counters.p);
     const float *d_table = nullptr;
@@ -811,6 +835,7 @@ void bang_index_destroy(bang_index *ix) {
     ix->csr.release();
     ix->skip.release();
     ix->retry_log.release();
+    ix->row_share.release();
     for (auto e : ix->ev)
         if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);
@@ -886,6 +911,15 @@ bang_status bang_search(bang_index *ix, const float *queries, int64_t nq, int32_
     if ((s = ix->q.reserve((size_t)nq * ix->dim))) return s;
     CU(cudaMemcpyAsync(ix->q.p, queries, sizeof(float) * nq * ix->dim, cudaMemcpyHostToDevice, st));
     if ((s = ensure_outputs(ix, nq, k, default_log_cap(ix, t)))) return s;
+    // the queries' finiteness (validation.py:17-19) is checked on the device,
+    // next to the search, instead of by a host pass over them
+    CU(cudaMemsetAsync(ix->counters.p + kCtrNonFinite, 0, sizeof(unsigned long long), st));
+    {
+        const int64_t cnt = nq * ix->dim;
+        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(cnt, 256), (int64_t)ix->sm_count * 8));
+        check_finite_kernel<<<blocks, 256, 0, st>>>(ix->q.p, cnt, ix->counters.p);
+        CU(cudaGetLastError());
+    }
     if ((s = enqueue_search(ix, ix->q.p, nq, k, t, bloom_entries, flags, ix->ids.p, ix->dists.p, ix->iters.p,
                             ix->shortf.p, st)))
         return s;
@@ -921,6 +955,7 @@ bang_status bang_search(bang_index *ix, const float *queries, int64_t nq, int32_
             if (wall) CU(cudaMemcpyAsync(wns.data(), ix->wall.p, sizeof(uint64_t) * nq, cudaMemcpyDeviceToHost, st));
             CU(cudaStreamSynchronize(st));
             if ((s = collect_stats(ix, ix->h_ctr))) return s;
+            if (ix->h_ctr[kCtrNonFinite]) return fail(BANG_E_PARAM, "queries contains non-finite values");
             if (ix->h_ctr[kCtrDebugFail])
                 return fail(BANG_E_STATE, "debug check failed: eager candidate disagrees with the post-merge worklist head");
             if (!ix->h_ctr[kCtrOverflow]) {
@@ -937,6 +972,7 @@ bang_status bang_search(bang_index *ix, const float *queries, int64_t nq, int32_
     }
     unsigned long long ctr[kCtrCount];
     if ((s = collect(ix, ctr))) return s;
+    if (ctr[kCtrNonFinite]) return fail(BANG_E_PARAM, "queries contains non-finite values");
     if (ctr[kCtrDebugFail])
         return fail(BANG_E_STATE, "debug check failed: eager candidate disagrees with the post-merge worklist head");
     std::vector<int32_t> it(nq);
@@ -1046,6 +1082,7 @@ void bang_options_default(bang_options *o) {
     o->bloom_clear = 1;
     o->l2_persist = 1;
     o->profile = 0;
+    o->bloom_direct = 1;
 }
 
 bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {

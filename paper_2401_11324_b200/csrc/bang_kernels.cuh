@@ -29,7 +29,8 @@ enum Counter {
     kCtrDebugFail = 6,
     kCtrT0 = 7,
     kCtrPhase0 = 8,  // 8 slots of per-phase SM cycles (BANG_PROFILE_PHASES)
-    kCtrCount = 16,
+    kCtrNonFinite = 16,  // bang_search: non-finite query values seen on the device
+    kCtrCount = 17,
 };
 
 // 24 warps x 32 lanes: leaves ptxas 80 registers per thread; shared memory
@@ -90,6 +91,10 @@ struct SearchParams {
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
     // one DRAM burst per gathered row)
     int32_t code_stride;
+    // search_split_kernel (bang_options.bloom_direct): bit w set when two
+    // distinct probes of node w's row share a Bloom slot at this z; rows
+    // without it take their pre-state bits from the fetch-or (nullptr: off)
+    const uint32_t *row_share;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

@@ -135,6 +135,38 @@ __device__ __noinline__ uint32_t split_replay(int rt, int deg, const RowProbes<P
     return fresh;
 }
 
+// ADC of this thread's staged code rows whose flag is set: acc = ((0 +
+// T[0][c0]) + T[1][c1]) + ... in f32 (engine.py:99-105); the lookups of a
+// chunk are issued before its sums
+template <int PL, int MV>
+__device__ __forceinline__ void split_adc(const bool (&on)[PL], int rt, const uint8_t *s_stage, const float *s_tab,
+                                          float (&acc)[PL]) {
+    constexpr int M = 16 * MV;
+    constexpr int CH = 16;  // table lookups issued ahead of their sums
+#pragma unroll
+    for (int r = 0; r < PL; ++r) {
+        acc[r] = 0.0f;
+        if (on[r]) {
+            uint4 code[MV];
+#pragma unroll
+            for (int v = 0; v < MV; ++v)
+                code[v] = *reinterpret_cast<const uint4 *>(s_stage + (rt + 64 * r) * M + 16 * v);
+#pragma unroll
+            for (int s0 = 0; s0 < M; s0 += CH) {
+                float e[CH];
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    const int s = s0 + q;
+                    const uint32_t word = u4_word(code[s >> 4], (s >> 2) & 3);
+                    e[q] = s_tab[s * 256 + ((word >> (8 * (s & 3))) & 0xFFu)];
+                }
+#pragma unroll
+                for (int q = 0; q < CH; ++q) acc[r] = __fadd_rn(acc[r], e[q]);
+            }
+        }
+    }
+}
+
 // Row warps: the row of node w -> keys in s_key[0, 64*PL) (SENTINEL for
 // slots past the degree and for neighbours the Bloom filter drops); their
 // minimum and fresh count in s_m (parity `par`).  rt = thread index among
@@ -145,7 +177,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
                                           uint32_t *bits, uint64_t *s_key, SplitMisc *s_m, int par,
                                           uint8_t *s_stage, uint8_t *s_tf) {
     constexpr int M = 16 * MV;
-    constexpr int CH = 16;  // table lookups issued ahead of their sums
     const int rw = rt >> 5, lane = rt & 31;
     // (p.profile == 2) row thread 0's cycles from entry to each stage, per hop
     const bool bk = p.profile == 2 && rt == 0;
@@ -153,6 +184,9 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #define SPLIT_STAMP(slot, dep) \
     if (bk) s_m->ph[slot] += (unsigned long long)(clock_after((int)(dep)) - c0);
     const int32_t *row = p.adj + (int64_t)w * p.adj_stride;
+    // in-row slot sharing of this row at this z (read with the row; no
+    // bitset: every row takes the exact pre-state path)
+    const uint32_t shw = p.row_share ? __ldg(p.row_share + (w >> 5)) : 0xFFFFFFFFu;
     uint32_t nid[PL];
     int deg;
     if (p.host_graph) {
@@ -167,12 +201,56 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         for (int r = 0; r < PL; ++r) nid[r] = rt + 64 * r < p.R ? (uint32_t)__ldg(row + rt + 64 * r) : 0u;
     }
     SPLIT_STAMP(0, nid[0] ^ (uint32_t)deg)
+    uint32_t p1[PL], p2[PL];
+    bool fresh[PL];
+    float acc[PL];
+    if (!((shw >> (w & 31)) & 1u)) {
+        // ---- no two probes of this row share a slot: batched test-then-set
+        // equals sequential test-and-set (bloom.py:135-151) and each
+        // fetch-or returns the pre-state of its own bits, so the sets go out
+        // at once (no pre-state read, no row barrier; setting the bits of a
+        // probe that turns out not fresh is a no-op -- both were set).  The
+        // code rows are staged by cp.async meanwhile and every probe's ADC
+        // runs while the fetch-ors return.
+        bool on[PL];
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            on[r] = rt + 64 * r < deg;
+            p1[r] = p2[r] = 0u;
+            if (on[r]) {
+                p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
+                p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
+                const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
+#pragma unroll
+                for (int v = 0; v < MV; ++v)
+                    __pipeline_memcpy_async(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v, 16);
+            }
+        }
+        __pipeline_commit();
+        uint32_t o1[PL], o2[PL];
+#pragma unroll
+        for (int r = 0; r < PL; ++r) {
+            o1[r] = o2[r] = 0u;
+            if (on[r]) {
+                o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
+                o2[r] = p2[r] != p1[r] ? atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
+            }
+        }
+        SPLIT_STAMP(1, p1[0])
+        __pipeline_wait_prior(0);  // this thread's own staged rows
+        split_adc<PL, MV>(on, rt, s_stage, s_tab, acc);
+        SPLIT_STAMP(3, __float_as_int(acc[0]))
+#pragma unroll
+        for (int r = 0; r < PL; ++r)
+            fresh[r] = on[r] && !(((o1[r] >> (p1[r] & 31)) & 1u) && ((o2[r] >> (p2[r] & 31)) & 1u));
+        SPLIT_STAMP(5, fresh[0])
+    } else {
     // ---- the Bloom slots and pre-state words (L2), then the code-row
     // gathers (HBM) staged into shared memory by cp.async.  The copies'
     // completion is tracked apart from the Bloom words', so the Bloom test
     // and the row's sets do not wait for HBM (issuing the copies first was
     // measured 7% slower: the Bloom words are the longer chain).
-    uint32_t p1[PL], p2[PL], wd1[PL], wd2[PL];
+    uint32_t wd1[PL], wd2[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
         p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
@@ -216,33 +294,9 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
         }
     }
-    // ---- ADC of the presumed-fresh neighbours while the fetch-ors return:
-    // acc = ((0 + T[0][c0]) + T[1][c1]) + ... in f32 (engine.py:99-105); the
-    // lookups of a chunk are issued before its sums
+    // ---- ADC of the presumed-fresh neighbours while the fetch-ors return
     __pipeline_wait_prior(0);  // this thread's own staged rows
-    float acc[PL];
-#pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        acc[r] = 0.0f;
-        if (pf[r]) {
-            uint4 code[MV];
-#pragma unroll
-            for (int v = 0; v < MV; ++v)
-                code[v] = *reinterpret_cast<const uint4 *>(s_stage + (rt + 64 * r) * M + 16 * v);
-#pragma unroll
-            for (int s0 = 0; s0 < M; s0 += CH) {
-                float e[CH];
-#pragma unroll
-                for (int q = 0; q < CH; ++q) {
-                    const int s = s0 + q;
-                    const uint32_t word = u4_word(code[s >> 4], (s >> 2) & 3);
-                    e[q] = s_tab[s * 256 + ((word >> (8 * (s & 3))) & 0xFFu)];
-                }
-#pragma unroll
-                for (int q = 0; q < CH; ++q) acc[r] = __fadd_rn(acc[r], e[q]);
-            }
-        }
-    }
+    split_adc<PL, MV>(pf, rt, s_stage, s_tab, acc);
     SPLIT_STAMP(3, __float_as_int(acc[0]))
     // ---- in-row slot sharing: a fetch-or found its bit set although the
     // pre-state lacked it -> another probe of this row set it first
@@ -257,7 +311,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     if (any_sh) s_m->coll = 1;
     split_bar(3, 64);
     SPLIT_STAMP(5, 0)
-    bool fresh[PL];
 #pragma unroll
     for (int r = 0; r < PL; ++r) fresh[r] = pf[r];
     if (s_m->coll) {
@@ -276,6 +329,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         const uint32_t f = split_replay<PL>(rt, deg, pr, s_stage, bits, s_tf);
 #pragma unroll
         for (int r = 0; r < PL; ++r) fresh[r] = (f >> r) & 1u;
+    }
     }
     // keys out; per-warp minimum (dist bits, then id: two 32-bit
     // reductions) and fresh count

@@ -400,7 +400,11 @@ class GraphSearcher(BaseEstimator):
         if k < 1 or k > self.t:
             raise ParameterError(f"k={k} must be in [1, t={self.t}]")
         data = getattr(queries, "data", queries)
-        q = as_float32_rows(check_matrix(data, "queries"))
+        # finiteness of f32 queries: checked by bang_search on the device
+        # (same message); other float types on the host before the cast (the
+        # device then also rejects values the f32 cast turned into inf)
+        arr = np.asarray(data)
+        q = as_float32_rows(check_matrix(arr, "queries", finite=arr.dtype != np.float32))
         nq = q.shape[0]
         if nq == 0:
             return SearchResult(np.zeros((0, k), np.int32), np.zeros((0, k), np.float32),

@@ -311,6 +311,23 @@ def test_batch_split_and_repeat_invariance():
         assert np.array_equal(r.iterations, r2.iterations)
 
 
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_non_finite_queries_rejected_on_device(bad):
+    """validation.py:17-19: f32 queries are checked by bang_search on the
+    device (the host skips its pass); same exception and message, and the
+    handle stays usable."""
+    g = gu.load("search_vamana_f32.npz")
+    s = _searcher_from_golden(g)
+    q = np.array(g["queries"], np.float32, copy=True)
+    q[len(q) // 2, -1] = bad
+    with pytest.raises(B.ParameterError, match="queries contains non-finite values"):
+        s.search(q)
+    with pytest.raises(B.ParameterError, match="queries contains non-finite values"):
+        s.search(q.astype(np.float64))  # host check before the f32 cast
+    res = s.search(g["queries"])
+    _assert_same(res, g["ids"], g["dists"], g["iterations"], gu.logs(g["log_offsets"], g["log_ids"]))
+
+
 def test_engine_equals_rerank_of_visit_log():
     """test_engine.py:137-149."""
     g = gu.load("search_vamana_r40_uneven.npz")
@@ -390,20 +407,22 @@ def test_search_matches_oracle_generated(seed, n, d, R, m, t, dtype):
     (17, 16_000, 128, 64, 32, 48, np.uint8, 1021),
     (18, 16_000, 96, 64, 48, 40, np.float32, 4099),
 ])
-@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch"])
+@pytest.mark.parametrize("flow", ["cta", "cta-summary", "split", "split-noprefetch", "split-exact"])
 def test_cta_kernel_bloom_replay_matches_oracle(seed, n, d, R, m, t, dtype, z, flow):
     """CTA kernels with small Bloom filters: most rows share slots, so the
     warp replay from pre-state bits (replay_row_warp) runs constantly.
     cta: search_cta_kernel (filter cleared per query; -summary: smem bitmap of
     written words instead); split: search_split_kernel (with and without the
-    head-row L2 prefetch)."""
+    head-row L2 prefetch; -exact: every row through the pre-state read, no
+    fetch-or-only rows)."""
     base, q, graph, cb, codes = _random_case(seed, n, d, R, m, 300, dtype)
     s = B.GraphSearcher(k=10, t=t, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
     if flow.startswith("cta"):
         s.set_kernel("cta", bloom_clear=0 if flow == "cta-summary" else 1)
     else:
-        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1)
+        s.set_kernel("split", row_prefetch=0 if flow == "split-noprefetch" else 1,
+                     bloom_direct=0 if flow == "split-exact" else 1)
     want = _oracle_search(q, graph, cb, codes, base, t, z)
     res = s.search(q)
     assert s.last_stats()["kernel"] == (2 if flow.startswith("cta") else 8)
@@ -449,6 +468,29 @@ def test_split_kernel_large_t_matches_oracle(shape, t):
     res = s.set_kernel("split").search(q)
     assert s.last_stats()["kernel"] == 8
     _same_as_oracle(res, _big_oracle(shape, t))
+
+
+@pytest.mark.parametrize("z", [20_011, 399_887])
+@pytest.mark.parametrize("direct", [0, 1])
+def test_split_bloom_direct_rows_match_oracle(z, direct):
+    """bloom_direct: rows without in-row slot sharing (a per-(index, z)
+    bitset) take their pre-state bits from the fetch-or, the others the
+    pre-state read + replay.  z = 20,011 flags about a third of the rows, so
+    one query mixes both paths; every 5th row repeats a neighbour id (always
+    shared).  A second z on the same index rebuilds the bitset."""
+    base, q, graph, cb, codes = _random_case(31, 20_000, 96, 64, 48, 200, np.float32)
+    adj = graph.adjacency.copy()
+    rows = np.arange(0, adj.shape[0], 5)
+    adj[rows, 7] = adj[rows, 3]
+    graph = B.GraphIndex(adj, graph.degrees, graph.medoid, graph.degree_bound, validate=False)
+    s = B.GraphSearcher(k=10, t=100, mode="in_memory", bloom_entries=z, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    s.set_kernel("split", bloom_direct=direct)
+    for zz in (z, 4099, z):
+        s.bloom_entries = zz
+        res = s.search(q)
+        assert s.last_stats()["kernel"] == 8
+        _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, 100, zz))
 
 
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
