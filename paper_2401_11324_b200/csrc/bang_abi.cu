@@ -145,8 +145,8 @@ struct bang_index {
     std::vector<int32_t> retry_q;
     int64_t retry_cap = 0;
     DevBuf<int32_t> retry_log;
-    // rows with in-row Bloom slot sharing at z = row_share_z (bloom_direct)
-    DevBuf<uint32_t> row_share;
+    // degree | in-row Bloom slot sharing << 31 at z = row_share_z (bloom_direct)
+    DevBuf<int32_t> row_share;
     int64_t row_share_z = 0;
 };
 
@@ -456,7 +456,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.row_prefetch = o.row_prefetch != 0;
-    p.row_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
+    p.deg_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -525,10 +525,8 @@ int64_t default_log_cap(const bang_index *ix, int t) {
 // (row_share_kernel), built on the first split search at this z.
 bang_status ensure_row_share(bang_index *ix, int64_t z, cudaStream_t st) {
     if (ix->row_share_z == z) return BANG_OK;
-    const int64_t words = ceil_div(ix->n, 32);
-    bang_status s = ix->row_share.reserve((size_t)words);
+    bang_status s = ix->row_share.reserve((size_t)ix->n);
     if (s) return s;
-    CU(cudaMemsetAsync(ix->row_share.p, 0, sizeof(uint32_t) * words, st));
     BloomGeom g;
     g.z = (uint64_t)z;
     g.magic = ~0ull / (uint64_t)z;

@@ -91,10 +91,11 @@ struct SearchParams {
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
     // one DRAM burst per gathered row)
     int32_t code_stride;
-    // search_split_kernel (bang_options.bloom_direct): bit w set when two
-    // distinct probes of node w's row share a Bloom slot at this z; rows
-    // without it take their pre-state bits from the fetch-or (nullptr: off)
-    const uint32_t *row_share;
+    // search_split_kernel (bang_options.bloom_direct): per node, its degree
+    // with bit 31 set when two distinct probes of its row share a Bloom slot
+    // at this z; rows without it take their pre-state bits from the
+    // fetch-or.  Read in place of deg (one load).  nullptr: off
+    const int32_t *deg_share;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

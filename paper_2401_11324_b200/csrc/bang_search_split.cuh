@@ -55,7 +55,7 @@ __device__ __forceinline__ void prefetch_row_l2(const SearchParams &p, uint32_t 
     asm volatile("prefetch.global.L2 [%0];" ::"l"(row) : "memory");
     if (((uintptr_t)row & 127u) + 4u * (uint32_t)p.R > 128u)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(row + p.R - 1) : "memory");
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.deg + v) : "memory");
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.deg_share ? p.deg_share + v : p.deg + v) : "memory");
 }
 // clock64 read that waits for v (a value loaded earlier): the profiler's
 // stamps must depend on the use they time
@@ -184,12 +184,18 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #define SPLIT_STAMP(slot, dep) \
     if (bk) s_m->ph[slot] += (unsigned long long)(clock_after((int)(dep)) - c0);
     const int32_t *row = p.adj + (int64_t)w * p.adj_stride;
-    // in-row slot sharing of this row at this z (read with the row; no
-    // bitset: every row takes the exact pre-state path)
-    const uint32_t shw = p.row_share ? __ldg(p.row_share + (w >> 5)) : 0xFFFFFFFFu;
     uint32_t nid[PL];
     int deg;
-    if (p.host_graph) {
+    bool shared = true;  // in-row slot sharing at this z (unknown: the exact path)
+    if (p.deg_share) {
+        // degree + sharing flag in one load (HBM; host-mapped rows too)
+        const int32_t v = __ldg(p.deg_share + w);
+        deg = v & 0x7FFFFFFF;
+        shared = v < 0;
+#pragma unroll
+        for (int r = 0; r < PL; ++r)
+            nid[r] = rt + 64 * r < p.R ? (uint32_t)(p.host_graph ? row[rt + 64 * r] : __ldg(row + rt + 64 * r)) : 0u;
+    } else if (p.host_graph) {
         // pinned, mapped host rows read over PCIe; with a [deg, 0, 0, 0]
         // header (p.row_hdr) degree and ids come in one coalesced read
         deg = p.row_hdr ? row[-4] : p.deg[w];
@@ -204,7 +210,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     uint32_t p1[PL], p2[PL];
     bool fresh[PL];
     float acc[PL];
-    if (!((shw >> (w & 31)) & 1u)) {
+    if (!shared) {
         // ---- no two probes of this row share a slot: batched test-then-set
         // equals sequential test-and-set (bloom.py:135-151) and each
         // fetch-or returns the pre-state of its own bits, so the sets go out
