@@ -237,9 +237,11 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #pragma unroll
         for (int r = 0; r < PL; ++r) {
             o1[r] = o2[r] = 0u;
+            // (o2 is not a copy of o1 when the slots coincide: a register
+            // move of the fetch-or result would wait for its round trip here)
             if (on[r]) {
                 o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
-                o2[r] = p2[r] != p1[r] ? atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
+                if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
             }
         }
         SPLIT_STAMP(1, p1[0])
@@ -248,7 +250,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         SPLIT_STAMP(3, __float_as_int(acc[0]))
 #pragma unroll
         for (int r = 0; r < PL; ++r)
-            fresh[r] = on[r] && !(((o1[r] >> (p1[r] & 31)) & 1u) && ((o2[r] >> (p2[r] & 31)) & 1u));
+            fresh[r] = on[r] && !(((o1[r] >> (p1[r] & 31)) & 1u) &&
+                                  (p2[r] == p1[r] || ((o2[r] >> (p2[r] & 31)) & 1u)));
         SPLIT_STAMP(5, fresh[0])
     } else {
     // ---- the Bloom slots and pre-state words (L2), then the code-row

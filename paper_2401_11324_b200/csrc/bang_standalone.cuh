@@ -63,56 +63,6 @@ __global__ void __launch_bounds__(32 * kShareWarps) row_share_kernel(const int32
     }
 }
 
-// validation.py:17-19 ("contains non-finite values") on the device, over the
-// queries bang_search has just uploaded: the host skips its own pass over
-// them.  One flag per warp that sees a NaN/inf.
-__global__ void check_finite_kernel(const float *__restrict__ x, int64_t count, unsigned long long *counters) {
-    bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-        bad |= !isfinite(__ldg(x + i));
-    if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicAdd(counters + kCtrNonFinite, 1ull);
-}
-
-// Rows with in-row Bloom slot sharing at Bloom size z (bloom.py:135-151's
-// "fresh candidates of one row share a slot", taken over ALL probes of the
-// row): bit w of `out` (zeroed by the caller) is set when two distinct
-// probes among node w's first deg[w] neighbours have a slot in common.  A
-// row without it behaves identically under batched and sequential
-// test-and-set, and each probe's fetch-or returns exactly the pre-state of
-// its own bits.  One warp per row; the row's 2*deg slots in shared memory,
-// every lane compares its own against all of them.  Built once per (index, z).
-constexpr int kShareWarps = 8;
-__global__ void __launch_bounds__(32 * kShareWarps) row_share_kernel(const int32_t *__restrict__ adj,
-                                                                     int64_t adj_stride,
-                                                                     const int32_t *__restrict__ deg,
-                                                                     int64_t n, int R, BloomGeom g,
-                                                                     uint32_t *__restrict__ out) {
-    extern __shared__ uint32_t s_slots[];  // [kShareWarps][2R]
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    uint32_t *sl = s_slots + wi * 2 * R;
-    for (int64_t w = (int64_t)blockIdx.x * kShareWarps + wi; w < n; w += (int64_t)gridDim.x * kShareWarps) {
-        const int d = min(max(deg[w], 0), R);
-        const int32_t *row = adj + w * adj_stride;
-        for (int j = lane; j < d; j += 32) {
-            const uint32_t id = (uint32_t)row[j];
-            sl[2 * j] = mod_z(fnv1a(id, kFnvOffset), g);
-            sl[2 * j + 1] = mod_z(fnv1a(id, kFnvOffsetH2), g);
-        }
-        __syncwarp();
-        bool dup = false;
-        for (int a = lane; a < 2 * d && !dup; a += 32) {
-            const uint32_t v = sl[a];
-            for (int b = 0; b < 2 * d; ++b)
-                if ((b >> 1) != (a >> 1) && sl[b] == v) {
-                    dup = true;
-                    break;
-                }
-        }
-        if (__any_sync(kFull, dup) && lane == 0) atomicOr(out + (w >> 5), 1u << (w & 31));
-        __syncwarp();
-    }
-}
-
 // -------------------------------------------------------------------------
 // Kernel 1 -- build_pq_dist_table (pq.py:284-319).  One CTA per query,
 // thread c = centroid c, subspaces in order; each subspace row (1 KB) is
