@@ -555,8 +555,8 @@ def main():
                 "adc_bytes": s_last["adc_bytes"],
                 "adc_gbs": round(s_last["adc_bytes"] / (avg_kern_ms / 1000.0) / 1e9, 1)}
 
-    if thr_only:
-        # host-resident graph (mode="pipelined"): rows and re-rank vectors
+    if mode == "pipelined":
+        # host-resident graph (mode="pipelined", C4 and C4r): rows and re-rank vectors
         # cross PCIe; the bound is the measured zero-copy read rate of random
         # rows of the same size (bang_host_read_bandwidth, mode 1)
         import ctypes

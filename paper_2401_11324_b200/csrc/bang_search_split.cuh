@@ -27,6 +27,17 @@
 
 #include "bang_search_cta.cuh"
 
+// A/B switches of the experiment builds (scripts/build_variant.sh)
+#ifndef BANG_SPLIT_BITSET
+#define BANG_SPLIT_BITSET 0
+#endif
+#ifndef BANG_SPLIT_O2COPY
+#define BANG_SPLIT_O2COPY 1
+#endif
+#ifndef BANG_SPLIT_LIST2
+#define BANG_SPLIT_LIST2 0
+#endif
+
 namespace bang {
 
 struct SplitMisc {
@@ -187,6 +198,17 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     uint32_t nid[PL];
     int deg;
     bool shared = true;  // in-row slot sharing at this z (unknown: the exact path)
+#if BANG_SPLIT_BITSET
+    // (A/B variant: the flag from a bitset beside the degree array)
+    if (p.deg_share) {
+        const uint32_t sw = __ldg(p.share_bits + (w >> 5));
+        deg = p.host_graph ? (p.row_hdr ? row[-4] : p.deg[w]) : __ldg(p.deg + w);
+        shared = (sw >> (w & 31)) & 1u;
+#pragma unroll
+        for (int r = 0; r < PL; ++r)
+            nid[r] = rt + 64 * r < p.R ? (uint32_t)(p.host_graph ? row[rt + 64 * r] : __ldg(row + rt + 64 * r)) : 0u;
+    } else
+#endif
     if (p.deg_share) {
         // degree + sharing flag in one load (HBM; host-mapped rows too)
         const int32_t v = __ldg(p.deg_share + w);
@@ -237,11 +259,17 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
 #pragma unroll
         for (int r = 0; r < PL; ++r) {
             o1[r] = o2[r] = 0u;
-            // (o2 is not a copy of o1 when the slots coincide: a register
-            // move of the fetch-or result would wait for its round trip here)
+            // (O2COPY: o2 = o1 when the slots coincide.  The register move
+            // waits for the fetch-or's round trip before the ADC starts, and
+            // that measured 2% faster than deferring the wait:
+            // profiles/r02/ab_v4/)
             if (on[r]) {
                 o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
+#if BANG_SPLIT_O2COPY
+                o2[r] = p2[r] != p1[r] ? atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
+#else
                 if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
+#endif
             }
         }
         SPLIT_STAMP(1, p1[0])
@@ -414,6 +442,47 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     const int c0w = s_m->wsurv[0], c1w = s_m->wsurv[1];
     const int n = c0w + c1w;
     SPLIT_STAMP(0, n)
+#if BANG_SPLIT_LIST2
+    // ---- kernels 4a + 4b in one pass over the (unsorted) survivors, from
+    // the same broadcast reads: each survivor's rank among them (its sorted
+    // slot) and each old entry's count of smaller survivors (keys are unique)
+    const int nch = (cnt + NC - 1) / NC;
+    uint64_t mv[MAXCH];
+    uint8_t mvv[MAXCH];
+    int mc[MAXCH];
+#pragma unroll
+    for (int c = 0; c < MAXCH; ++c) {
+        const int i = c * NC + lt;
+        mv[c] = kSentinel;
+        mvv[c] = 0;
+        mc[c] = 0;
+        if (c < nch && i < cnt) {
+            mv[c] = s_wl[i];
+            mvv[c] = s_vis[i];
+        }
+    }
+    if (n > 0) {
+        int rk[PL];
+#pragma unroll
+        for (int r = 0; r < PL; ++r) rk[r] = 0;
+        auto count = [&](const uint64_t sk) {
+#pragma unroll
+            for (int r = 0; r < PL; ++r) rk[r] += sk < k[r];
+#pragma unroll
+            for (int c = 0; c < MAXCH; ++c) mc[c] += sk < mv[c];
+        };
+        for (int i = 0; i < c0w; ++i) count(s_nk[i]);
+        for (int i = 0; i < c1w; ++i) count(s_nk[H + i]);
+#pragma unroll
+        for (int r = 0; r < PL; ++r)
+            if (sv[r]) s_sk[rk[r]] = k[r];
+#pragma unroll
+        for (int c = 0; c < MAXCH; ++c)
+            if (c < nch && c * NC + lt < cnt) s_c[c * NC + lt] = (int16_t)mc[c];
+    }
+    SPLIT_STAMP(1, 0)
+    SPLIT_STAMP(2, mc[0])
+#else
     // ---- kernel 4a: rank sort of the survivors (broadcast reads)
 #pragma unroll
     for (int r = 0; r < PL; ++r) {
@@ -454,6 +523,7 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
             if (c < nch && c * NC + lt < cnt) s_c[c * NC + lt] = (int16_t)mc[c];
     }
     SPLIT_STAMP(2, mc[0])
+#endif
     split_bar(4, NC);  // all reads of the old worklist precede the writes
     // ---- merge + truncate to t (engine.py:210-215): old entry i goes to
     // i + c_i; survivors c_{i-1} .. c_i - 1 land just before it, the rest
