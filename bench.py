@@ -609,9 +609,10 @@ def main():
         if s_last.get("kernel") == 8:  # search_split_kernel: row thread 0 / list thread 0 per hop
             prof = searcher.index_.options().get("profile", 0)
             names = {2: ["row_ids", "bloom_words", "pre_bar", "adc", "unused", "coll_bar", "row_end"],
-                     3: ["compact", "sort", "merge_reads", "merge_writes", "list_end"]}.get(
+                     3: ["compact", "sort", "merge_reads", "merge_writes", "list_end", "head_won_frac",
+                         "survivors_per_hop"]}.get(
                 prof, ["row_chain", "list_step", "row_wait_at_hop_barrier", "list_wait_at_hop_barrier"])
-            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 1) for i, nm in enumerate(names)}
+            out["phase_cycles_per_iteration"] = {nm: round(pc[i] / it, 3) for i, nm in enumerate(names)}
             out["phase_cycles_per_iteration"]["prologue_epilogue_per_query"] = round(pc[7] / max(1, nq), 1)
         elif s_last.get("kernel") == 2:  # search_cta_kernel: thread 0's cycles
             names = ["bloom_load", "zero_sync", "adc_reduce", "coll_sync", "winner_prefetch", "sort", "merge"]

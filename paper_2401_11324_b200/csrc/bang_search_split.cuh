@@ -35,7 +35,10 @@
 #define BANG_SPLIT_O2COPY 1
 #endif
 #ifndef BANG_SPLIT_LIST2
-#define BANG_SPLIT_LIST2 0
+#define BANG_SPLIT_LIST2 1
+#endif
+#ifndef BANG_SPLIT_HEADPF
+#define BANG_SPLIT_HEADPF 0
 #endif
 
 namespace bang {
@@ -53,6 +56,7 @@ struct SplitMisc {
     int opos;                    // list warps: old position of okey (cnt if none)
     int coll;                    // row warps: in-row slot sharing seen
     long long qi;
+    unsigned long long pfh;      // list warps: head whose neighbours' code rows went to L2 (HEADPF)
     unsigned long long ph[8];  // phase profiler
 };
 static_assert(sizeof(SplitMisc) <= 256, "SplitMisc must fit its 256-byte smem slot");
@@ -594,7 +598,29 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         // the head may be the next winner: its row to L2
         if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
     }
+#if BANG_SPLIT_HEADPF
+    // A head that stays the head (its adjacency row went to L2 a hop ago,
+    // so this read hits) gets its neighbours' code rows prefetched to L2:
+    // if it wins the next hop, the row warps' gathers hit L2.  Once per head.
+    if (!p.host_graph) {
+        split_bar(4, NC);  // the published head
+        const uint64_t hk2 = s_m->head[nxt];
+        if (hk2 != kSentinel && hk2 == head && s_m->pfh != hk2) {
+            const int32_t *hrow = p.adj + (int64_t)key_id(hk2) * p.adj_stride;
+            for (int j = lt; j < p.R; j += NC) {
+                const int32_t id = __ldg(hrow + j);
+                if (id >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.codes + (int64_t)id * p.code_stride) : "memory");
+            }
+            split_bar(4, NC);  // every list thread has read pfh
+            if (lt == 0) s_m->pfh = hk2;
+        }
+    }
+#endif
     SPLIT_STAMP(4, 0)
+    if (bk) {  // hop statistics: expansions of the old head, survivors merged
+        s_m->ph[5] += won_head;
+        s_m->ph[6] += (unsigned long long)n;
+    }
 #undef SPLIT_STAMP
 }
 
@@ -786,6 +812,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             s_m->hpos[0] = 1;
             s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
             s_m->cnt[0] = 1;
+            s_m->pfh = kSentinel;
         }
         if (p.profile && tid == 0) {
             const long long now_ = clock64();
