@@ -161,6 +161,7 @@ struct Plan {
     int kernel = kKGeneric;
     int npl = 2, sub = 0, mv = 0;
     int off_code = 0;
+    int off_hrow = 0;         // split kernel: staged head row ids
     int off_row = 0;          // CTA kernel: staged host-mapped row (header + ids)
     int off_dup = 0;
     int nt = 0;               // threads per CTA of the CTA kernels
@@ -227,6 +228,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         // staged code rows (16*MV bytes each); the replay records reuse it
         pl.off_dup = take(std::max<int64_t>(16LL * mv * srpad, 10LL * srpad));
         pl.off_alive = take(srpad);        // replay output
+        pl.off_hrow = take(4LL * srpad);   // the head's row ids, staged by the list warps
         pl.off_acc = take(256);            // SplitMisc
         pl.off_vis = take(t);
         pl.off_tab = take(tab_bytes);
@@ -456,6 +458,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_dup = pl.off_dup;
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
+    p.off_hrow = pl.off_hrow;
     p.row_prefetch = o.row_prefetch != 0;
     p.deg_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
     p.share_bits = p.deg_share ? ix->share_bits.p : nullptr;

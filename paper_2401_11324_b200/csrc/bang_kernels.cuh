@@ -88,6 +88,8 @@ struct SearchParams {
     int32_t host_graph;
     // search_split_kernel: the row keys (double-buffered) at off_code
     int32_t off_code;
+    // search_split_kernel: the head's row ids staged by the list warps
+    int32_t off_hrow;
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
     // one DRAM burst per gathered row)
     int32_t code_stride;

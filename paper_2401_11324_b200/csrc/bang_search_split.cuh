@@ -40,6 +40,9 @@
 #ifndef BANG_SPLIT_HEADPF
 #define BANG_SPLIT_HEADPF 0
 #endif
+#ifndef BANG_SPLIT_HEADROW
+#define BANG_SPLIT_HEADROW 1
+#endif
 
 namespace bang {
 
@@ -57,6 +60,8 @@ struct SplitMisc {
     int coll;                    // row warps: in-row slot sharing seen
     long long qi;
     unsigned long long pfh;      // list warps: head whose neighbours' code rows went to L2 (HEADPF)
+    uint32_t hid;                // HEADROW: node whose row ids are staged in s_hrow (~0u: none)
+    int32_t hdeg;                // HEADROW: its deg_share word
     unsigned long long ph[8];  // phase profiler
 };
 static_assert(sizeof(SplitMisc) <= 256, "SplitMisc must fit its 256-byte smem slot");
@@ -190,7 +195,7 @@ __device__ __forceinline__ void split_adc(const bool (&on)[PL], int rt, const ui
 template <int PL, int MV>
 __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int rt, const float *s_tab,
                                           uint32_t *bits, uint64_t *s_key, SplitMisc *s_m, int par,
-                                          uint8_t *s_stage, uint8_t *s_tf) {
+                                          uint8_t *s_stage, uint8_t *s_tf, const int32_t *s_hrow, bool hop1) {
     constexpr int M = 16 * MV;
     const int rw = rt >> 5, lane = rt & 31;
     // (p.profile == 2) row thread 0's cycles from entry to each stage, per hop
@@ -202,6 +207,30 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     uint32_t nid[PL];
     int deg;
     bool shared = true;  // in-row slot sharing at this z (unknown: the exact path)
+    bool pre = false;
+#if BANG_SPLIT_HEADROW
+    // The list warps staged the published head's row ids + deg_share word
+    // (68% of hops expand the old head): no adjacency read then.  Every hop
+    // h >= 1 the row warps arrive on barrier 5 once they hold s_hrow, so the
+    // list warps may overwrite it (they sync on 5 late in the hop).
+    if (hop1 && p.deg_share && !p.host_graph) {
+        uint32_t dep = 0;
+        if (s_m->hid == w) {
+            pre = true;
+            const int32_t v = s_m->hdeg;
+            deg = v & 0x7FFFFFFF;
+            shared = v < 0;
+#pragma unroll
+            for (int r = 0; r < PL; ++r) {
+                nid[r] = rt + 64 * r < p.R ? (uint32_t)s_hrow[rt + 64 * r] : 0u;
+                dep ^= nid[r];
+            }
+        }
+        asm volatile("bar.arrive 5, 128;" ::"r"(dep) : "memory");
+    }
+    if (pre) {
+    } else
+#endif
 #if BANG_SPLIT_BITSET
     // (A/B variant: the flag from a bitset beside the degree array)
     if (p.deg_share) {
@@ -406,7 +435,8 @@ template <int PL>
 __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64_t *s_wl, uint8_t *s_vis,
                                            const uint64_t *s_key, uint64_t *s_nk, uint64_t *s_sk, int16_t *s_c,
                                            int16_t *s_spos, SplitMisc *s_m, int nxt, uint64_t winner,
-                                           uint64_t head, uint64_t thr, int cnt, int hpos, int32_t *log, int iters) {
+                                           uint64_t head, uint64_t thr, int cnt, int hpos, int32_t *log, int iters,
+                                           int32_t *s_hrow) {
     constexpr int NC = 64;      // list threads
     constexpr int MAXCH = 4;    // worklists up to 4*NC entries (checked on the host)
     constexpr int H = 32 * PL;  // survivors region per list warp
@@ -598,6 +628,35 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         // the head may be the next winner: its row to L2
         if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
     }
+#if BANG_SPLIT_HEADROW
+    // stage the published head's row ids + deg_share word for the row warps
+    // (used when it wins the next hop); the loads run in the list warps'
+    // slack before the hop barrier
+    if (p.deg_share && !p.host_graph) {
+        split_bar(4, NC);  // the published head
+        const uint64_t hk2 = s_m->head[nxt];
+        int32_t ids[PL];
+        int32_t hv = 0;
+        uint32_t hid = 0xFFFFFFFFu;
+#pragma unroll
+        for (int r = 0; r < PL; ++r) ids[r] = 0;
+        if (hk2 != kSentinel) {
+            hid = key_id(hk2);
+            const int32_t *hrow = p.adj + (int64_t)hid * p.adj_stride;
+#pragma unroll
+            for (int r = 0; r < PL; ++r)
+                if (lt + 64 * r < p.R) ids[r] = __ldg(hrow + lt + 64 * r);
+            if (lt == 0) hv = __ldg(p.deg_share + hid);
+        }
+        split_bar(5, 128);  // the row warps hold this hop's s_hrow
+#pragma unroll
+        for (int r = 0; r < PL; ++r) s_hrow[lt + 64 * r] = ids[r];
+        if (lt == 0) {
+            s_m->hdeg = hv;
+            s_m->hid = hid;
+        }
+    }
+#endif
 #if BANG_SPLIT_HEADPF
     // A head that stays the head (its adjacency row went to L2 a hop ago,
     // so this read hits) gets its neighbours' code rows prefetched to L2:
@@ -775,6 +834,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
     int16_t *s_spos = s_c + ((p.t + 7) & ~7);                              // [RPAD]
     uint8_t *s_stage = smem + p.off_dup;  // [RPAD][M] staged code rows / replay records
     uint8_t *s_tf = smem + p.off_alive;                                   // [RPAD]
+    int32_t *s_hrow = reinterpret_cast<int32_t *>(smem + p.off_hrow);     // [RPAD] staged head row
     uint8_t *s_vis = smem + p.off_vis;
     float *s_tab = reinterpret_cast<float *>(smem + p.off_tab);
     SplitMisc *s_m = reinterpret_cast<SplitMisc *>(smem + p.off_acc);
@@ -813,6 +873,7 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
             s_m->cnt[0] = 1;
             s_m->pfh = kSentinel;
+            s_m->hid = 0xFFFFFFFFu;
         }
         if (p.profile && tid == 0) {
             const long long now_ = clock64();
@@ -841,10 +902,10 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             const long long c0 = prof ? clock64() : 0;
             if (roww) {
                 split_row<PL, MV>(p, key_id(winner), tid, s_tab, bits, s_key + (par ^ 1) * RPAD, s_m, par ^ 1,
-                                  s_stage, s_tf);
+                                  s_stage, s_tf, s_hrow, iters > 0);
             } else if (iters > 0) {
                 split_list<PL>(p, tid - 64, s_wl, s_vis, s_key + par * RPAD, s_nk, s_sk, s_c, s_spos, s_m, par ^ 1,
-                               winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters);
+                               winner, head, thr, s_m->cnt[par], s_m->hpos[par], log, iters, s_hrow);
             }
             long long c1 = 0;
             if (prof) {

@@ -183,6 +183,23 @@ def _save_cached(path, arrays, log):
         shutil.rmtree(tmp, ignore_errors=True)
 
 
+def _ck_has(ck, *names) -> bool:
+    return all(os.path.exists(os.path.join(ck, k + ".npy")) for k in names)
+
+
+def _ck_load(ck, name):
+    return np.load(os.path.join(ck, name + ".npy"), mmap_mode="r")
+
+
+def _ck_save(ck, **arrays) -> None:
+    """Each array written to a temporary name, then renamed: a checkpoint
+    file is complete or absent."""
+    for k, a in arrays.items():
+        tmp = os.path.join(ck, k + ".tmp.npy")
+        np.save(tmp, np.asarray(a))
+        os.replace(tmp, os.path.join(ck, k + ".npy"))
+
+
 def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache_dir: str | None = None,
                     log=print, load_only: bool = False):
     """Returns dict(base, queries, graph, codebook, codes, gt_ids, gt_dists, meta).
@@ -203,15 +220,38 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         if os.path.isdir(path) or load_only:
             return _load_cached(path, name, meta, log)
     t0 = time.time()
-    base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed,
-                                     out_dtype=np.uint8 if dt == "u8" else np.float32)
-    if dt == "u8":
-        queries = queries.astype(np.float32)
+    # the partitioned (C4-size) builds checkpoint every stage to disk so a
+    # build longer than one GPU session resumes where it stopped
+    ck = None
+    if name in PARTITIONED:
+        ck = os.path.join(cache_dir or "/tmp", f"bang_{name}_ckpt_{_key(name, seed, nq_total)}")
+        os.makedirs(ck, exist_ok=True)
+    if ck and _ck_has(ck, "base", "queries"):
+        base, queries = _ck_load(ck, "base"), np.asarray(_ck_load(ck, "queries"))
+        log(f"[bench_data] {name}: data from checkpoint {ck}")
+    else:
+        base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed,
+                                         out_dtype=np.uint8 if dt == "u8" else np.float32)
+        if dt == "u8":
+            queries = queries.astype(np.float32)
+        if ck:
+            _ck_save(ck, base=base, queries=queries)
     t1 = time.time()
     if name in PARTITIONED:
         from .graph_build import build_graph_partitioned
-        cb = train_codebook(base, m=m, iters=15, seed=seed)
-        codes = encode(base, cb)
+        if _ck_has(ck, "centroids", "sub_sizes", "codes"):
+            cat, sizes = np.asarray(_ck_load(ck, "centroids")), [int(v) for v in _ck_load(ck, "sub_sizes")]
+            cents, pos = [], 0
+            for sz in sizes:
+                cents.append(cat[pos:pos + 256 * sz].reshape(256, sz))
+                pos += 256 * sz
+            cb = PQCodebook(dim=dim, subspace_sizes=sizes, centroids=cents)
+            codes = CompressedVectors(np.asarray(_ck_load(ck, "codes")))
+        else:
+            cb = train_codebook(base, m=m, iters=15, seed=seed)
+            codes = encode(base, cb)
+            _ck_save(ck, centroids=cb.concatenated(), sub_sizes=np.asarray(cb.subspace_sizes, np.int32),
+                     codes=codes.codes)
         t2 = time.time()
         cfg = PARTITIONED[name]
 
@@ -219,8 +259,14 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
             return refine_with_search(base[members], g, cb, CompressedVectors(codes.codes[members]), R,
                                       t=t_ref, log=log)
 
-        graph = build_graph_partitioned(base, degree_bound=R, parts=cfg["parts"], overlap=cfg["overlap"],
-                                        refine_fn=refine_fn, refine=cfg["refine"], seed=seed, log=log)
+        if _ck_has(ck, "adjacency", "degrees", "medoid"):
+            graph = GraphIndex(_ck_load(ck, "adjacency"), np.asarray(_ck_load(ck, "degrees")),
+                               int(_ck_load(ck, "medoid")), R, validate=False)
+        else:
+            graph = build_graph_partitioned(base, degree_bound=R, parts=cfg["parts"], overlap=cfg["overlap"],
+                                            refine_fn=refine_fn, refine=cfg["refine"], seed=seed, log=log,
+                                            ckpt_dir=ck)
+            _ck_save(ck, adjacency=graph.adjacency, degrees=graph.degrees, medoid=np.int64(graph.medoid))
         t3 = time.time()
         t2, t3 = t3 - (t2 - t1), t3  # report graph time apart from PQ time
     else:
@@ -244,7 +290,12 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         graph = GraphIndex(adj, deg, med, R, validate=False)
         codes = CompressedVectors(np.ascontiguousarray(codes.codes[perm]))
         log(f"[bench_data] {name}: relabelled in k-means partition order ({time.time() - t3:.1f}s)")
-    gt_ids, gt_d = brute_force_knn(base, queries, 10)
+    if ck and _ck_has(ck, "gt_ids", "gt_dists"):
+        gt_ids, gt_d = np.asarray(_ck_load(ck, "gt_ids")), np.asarray(_ck_load(ck, "gt_dists"))
+    else:
+        gt_ids, gt_d = brute_force_knn(base, queries, 10)
+        if ck:
+            _ck_save(ck, gt_ids=gt_ids, gt_dists=gt_d)
     t4 = time.time()
     log(f"[bench_data] {name}: data {t1 - t0:.1f}s graph {t2 - t1:.1f}s pq {t3 - t2:.1f}s gt {t4 - t3:.1f}s"
         f" (mean degree {graph.degrees.mean():.1f})")

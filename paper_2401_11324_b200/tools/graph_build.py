@@ -12,6 +12,8 @@ construction, not the hot path.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .._dev import torch_device
@@ -407,7 +409,7 @@ def refine_graph(x, adj, deg, visit_fn, R: int, sigma: float = 1.2, chunk: int =
 
 def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overlap: int = 2,
                             sigma: float = 1.2, refine_fn=None, refine=(), seed: int = 0,
-                            merge_chunk: int = 1 << 19, device=None, log=print) -> GraphIndex:
+                            merge_chunk: int = 1 << 19, device=None, log=print, ckpt_dir=None) -> GraphIndex:
     """Graph of a base set too large for one build in HBM (C4: 100M x 128 u8).
 
     DiskANN-style partitioned construction: k-means on a sample gives
@@ -417,7 +419,9 @@ def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overl
     a point's neighbour lists from its partitions are merged with one
     RobustPrune(sigma) over their union (exact distances).  Shared points
     connect the partitions.  Memory: the base stays in host RAM (u8 or f32)
-    plus one partition and an (n, overlap*R) int32 candidate table."""
+    plus one partition and an (n, overlap*R) int32 candidate table.
+    ckpt_dir: the assignment, the candidate table (a memory-mapped .npy)
+    and the finished partitions are kept there; a later call resumes."""
     import gc
     import time
     import torch
@@ -426,27 +430,49 @@ def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overl
     n, d = xn.shape
     R = int(degree_bound)
     t0 = time.time()
-    rng = np.random.default_rng(seed)
-    samp = np.sort(rng.choice(n, size=min(n, 1 << 20), replace=False))
-    xs = torch.from_numpy(np.ascontiguousarray(xn[samp], dtype=np.float32)).to(dev)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = False
-    try:
-        cent = kmeans(xs, parts, seed=seed)
-        del xs
-        assign = np.empty((n, overlap), np.int32)
-        for lo in range(0, n, 1 << 22):
-            xb = torch.from_numpy(np.ascontiguousarray(xn[lo:lo + (1 << 22)])).to(dev).float()
-            assign[lo:lo + (1 << 22)] = _nearest_centroids(xb, cent, overlap).to(torch.int32).cpu().numpy()
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    ck = (lambda k: os.path.join(ckpt_dir, k)) if ckpt_dir else None
+    if ckpt_dir:
+        os.makedirs(ckpt_dir, exist_ok=True)
+    if ck and os.path.exists(ck("assign.npy")):
+        assign = np.load(ck("assign.npy"))
+    else:
+        rng = np.random.default_rng(seed)
+        samp = np.sort(rng.choice(n, size=min(n, 1 << 20), replace=False))
+        xs = torch.from_numpy(np.ascontiguousarray(xn[samp], dtype=np.float32)).to(dev)
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = False
+        try:
+            cent = kmeans(xs, parts, seed=seed)
+            del xs
+            assign = np.empty((n, overlap), np.int32)
+            for lo in range(0, n, 1 << 22):
+                xb = torch.from_numpy(np.ascontiguousarray(xn[lo:lo + (1 << 22)])).to(dev).float()
+                assign[lo:lo + (1 << 22)] = _nearest_centroids(xb, cent, overlap).to(torch.int32).cpu().numpy()
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = prev
+        if ck:
+            np.save(ck("assign.tmp.npy"), assign)
+            os.replace(ck("assign.tmp.npy"), ck("assign.npy"))
     log(f"[graph_build] partitioned: {parts} parts x {overlap}-way, assignment {time.time() - t0:.1f}s")
     # members of each partition (stable order), and which of a point's slots it fills
     flat = assign.ravel()
     order = np.argsort(flat, kind="stable")
     bounds = np.searchsorted(flat[order], np.arange(parts + 1))
-    cand = np.full((n, overlap * R), -1, np.int32)
+    done = set()
+    if ck:
+        if os.path.exists(ck("cand.npy")):
+            cand = np.load(ck("cand.npy"), mmap_mode="r+")
+            if os.path.exists(ck("done.txt")):
+                done = {int(v) for v in open(ck("done.txt")).read().split()}
+        else:
+            cand = np.lib.format.open_memmap(ck("cand.npy"), mode="w+", dtype=np.int32, shape=(n, overlap * R))
+            cand[:] = -1
+        log(f"[graph_build] checkpoint {ckpt_dir}: partitions done {sorted(done)}")
+    else:
+        cand = np.full((n, overlap * R), -1, np.int32)
     for p in range(parts):
+        if p in done:
+            continue
         t1 = time.time()
         sel = order[bounds[p]:bounds[p + 1]]
         members, slot = sel // overlap, sel % overlap
@@ -461,6 +487,10 @@ def build_graph_partitioned(base, degree_bound: int = 64, parts: int = 16, overl
             m_ = slot == j
             cand[members[m_], j * R:(j + 1) * R] = glob[m_]
         del g, adj, glob
+        if ck:
+            cand.flush()
+            with open(ck("done.txt"), "a") as f:
+                f.write(f"{p}\n")
         # the partition's device tensors must be gone before the next one
         # (a reference cycle would otherwise keep ~10 GB per partition alive)
         gc.collect()

@@ -169,3 +169,31 @@ def test_partitioned_build_is_valid_and_as_good_as_monolithic():
         return np.mean([len(set(a) & set(c)) / 10 for a, c in zip(r["ids"], gt)])
 
     assert rec(gp) >= rec(gm) - 0.03
+
+
+def test_partitioned_build_resumes_from_checkpoint(tmp_path):
+    """The C4 builder checkpoints the assignment, the candidate table and each
+    finished partition: a run stopped after some partitions resumes and gives
+    the graph of an uninterrupted run (one device, deterministic CPU ops)."""
+    b, _ = gaussian_mixture(6_000, 0, 16, clusters=60, seed=5, out_dtype=np.uint8)
+    full = gb.build_graph_partitioned(b, degree_bound=12, parts=3, overlap=2, device="cpu", merge_chunk=2000,
+                                      ckpt_dir=str(tmp_path / "a"))
+    ck = tmp_path / "b"
+    ck.mkdir()
+    calls = []
+
+    def stop_after_two(members, g, t):
+        calls.append(t)
+        if len(calls) == 3:
+            raise KeyboardInterrupt  # the session ends during partition 3
+        return g
+    with pytest.raises(KeyboardInterrupt):
+        gb.build_graph_partitioned(b, degree_bound=12, parts=3, overlap=2, device="cpu", merge_chunk=2000,
+                                   refine_fn=stop_after_two, refine=(1,), ckpt_dir=str(ck))
+    assert open(ck / "done.txt").read().split() == ["0", "1"]
+    redo = []
+    resumed = gb.build_graph_partitioned(b, degree_bound=12, parts=3, overlap=2, device="cpu", merge_chunk=2000,
+                                         refine_fn=lambda m, g, t: redo.append(t) or g, refine=(1,),
+                                         ckpt_dir=str(ck))
+    assert redo == [1]  # only the unfinished partition is rebuilt
+    assert np.array_equal(resumed.adjacency, full.adjacency) and np.array_equal(resumed.degrees, full.degrees)
