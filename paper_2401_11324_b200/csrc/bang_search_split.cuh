@@ -43,8 +43,61 @@
 #ifndef BANG_SPLIT_HEADROW
 #define BANG_SPLIT_HEADROW 1
 #endif
+#ifndef BANG_SPLIT_L2HINT
+#define BANG_SPLIT_L2HINT 1
+#endif
 
 namespace bang {
+
+// L2 residency of the per-query Bloom filters.  A query's ~17 K fetch-ors hit
+// random words of its 50 KB filter over ~0.5 ms while ~0.6 GB of code rows,
+// adjacency rows and vectors stream through the 126 MB L2; with default
+// priorities half of the fetch-ors missed L2 (ncu: 109 M of 220 M atomic
+// sectors), putting a DRAM round trip on every hop's critical path.  The
+// filter's accesses carry an evict_last policy, the code-row gathers
+// evict_first (BANG_SPLIT_L2HINT; the launch's persisting access window
+// sizes the evict_last set).
+#if BANG_SPLIT_L2HINT
+__device__ __forceinline__ uint64_t l2_keep() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_stream() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint32_t bloom_or(uint32_t *a, uint32_t v) {
+    uint32_t o;
+    asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(l2_keep()) : "memory");
+    return o;
+}
+__device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) {
+    uint32_t o;
+    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(l2_keep()) : "memory");
+    return o;
+}
+__device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) {
+    asm volatile("st.global.cg.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_keep()) : "memory");
+}
+__device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) {
+    asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w), "l"(l2_keep())
+                 : "memory");
+}
+__device__ __forceinline__ void code_copy16(void *dst, const void *src) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "l"(l2_stream())
+                 : "memory");
+}
+#else
+__device__ __forceinline__ uint32_t bloom_or(uint32_t *a, uint32_t v) { return atomicOr(a, v); }
+__device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) { return __ldcg(a); }
+__device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) { __stcg(a, v); }
+__device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) { __stcg(a, v); }
+__device__ __forceinline__ void code_copy16(void *dst, const void *src) { __pipeline_memcpy_async(dst, src, 16); }
+#endif
 
 struct SplitMisc {
     unsigned long long rmin[2][2];  // [parity][row warp]: min key of the row's fresh neighbours
@@ -284,7 +337,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
                 const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
 #pragma unroll
                 for (int v = 0; v < MV; ++v)
-                    __pipeline_memcpy_async(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v, 16);
+                    code_copy16(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v);
             }
         }
         __pipeline_commit();
@@ -297,11 +350,11 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             // that measured 2% faster than deferring the wait:
             // profiles/r02/ab_v4/)
             if (on[r]) {
-                o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
+                o1[r] = bloom_or(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
 #if BANG_SPLIT_O2COPY
-                o2[r] = p2[r] != p1[r] ? atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
+                o2[r] = p2[r] != p1[r] ? bloom_or(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
 #else
-                if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
+                if (p2[r] != p1[r]) o2[r] = bloom_or(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
 #endif
             }
         }
@@ -327,8 +380,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
         if (rt + 64 * r < deg) {
             p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
             p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
-            wd1[r] = __ldcg(bits + (p1[r] >> 5));
-            wd2[r] = __ldcg(bits + (p2[r] >> 5));
+            wd1[r] = bloom_ld(bits + (p1[r] >> 5));
+            wd2[r] = bloom_ld(bits + (p2[r] >> 5));
         }
     }
 #pragma unroll
@@ -337,7 +390,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
 #pragma unroll
             for (int v = 0; v < MV; ++v)
-                __pipeline_memcpy_async(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v, 16);
+                code_copy16(s_stage + (rt + 64 * r) * M + 16 * v, crow + 16 * v);
         }
     }
     __pipeline_commit();
@@ -360,8 +413,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     for (int r = 0; r < PL; ++r) {
         o1[r] = o2[r] = 0u;
         if (pf[r]) {
-            o1[r] = atomicOr(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
-            if (p2[r] != p1[r]) o2[r] = atomicOr(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
+            o1[r] = bloom_or(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
+            if (p2[r] != p1[r]) o2[r] = bloom_or(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
         }
     }
     // ---- ADC of the presumed-fresh neighbours while the fetch-ors return
@@ -706,7 +759,7 @@ __device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qi
     for (int i = tid; i < t; i += NT) s_vis[i] = 0;
     {   // the filter starts empty (whole-line stores)
         uint4 *b4 = reinterpret_cast<uint4 *>(bits);
-        for (int i = tid; i < n4; i += NT) __stcg(b4 + i, make_uint4(0u, 0u, 0u, 0u));
+        for (int i = tid; i < n4; i += NT) bloom_st4(b4 + i, make_uint4(0u, 0u, 0u, 0u));
     }
     __syncthreads();
     // kernel 1 for this query into shared memory (pq.py:284-296); the
@@ -738,10 +791,10 @@ __device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qi
         const uint32_t w1 = mp1 >> 5, w2 = mp2 >> 5;
         const uint32_t b1 = 1u << (mp1 & 31), b2 = 1u << (mp2 & 31);
         if (w1 == w2) {
-            __stcg(bits + w1, b1 | b2);
+            bloom_st(bits + w1, b1 | b2);
         } else {
-            __stcg(bits + w1, b1);
-            __stcg(bits + w2, b2);
+            bloom_st(bits + w1, b1);
+            bloom_st(bits + w2, b2);
         }
     }
     __syncthreads();
