@@ -19,6 +19,11 @@
 
 #include "bang_kernels.cuh"
 
+// A/B switch (scripts/build_variant.sh): re-rank rows staged by cp.async
+#ifndef BANG_RERANK_ASYNC
+#define BANG_RERANK_ASYNC 1
+#endif
+
 namespace bang {
 
 struct CtaMisc {
@@ -51,11 +56,25 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
     const uint8_t *vec = static_cast<const uint8_t *>(p.vectors);
     for (int base = 0; base < iters; base += ch) {
         const int nr = min(ch, iters - base);
+        // the rows' 16-byte pieces by cp.async (no register round trip); the
+        // log reads of 8 pieces are in flight together, so a chunk costs a few
+        // L2 round trips and one HBM round trip, not one of each per piece
+#if BANG_RERANK_ASYNC
+#pragma unroll 8
+        for (int u = tid; u < nr * upr; u += NT) {
+            const int r = u / upr, c = u - r * upr;
+            const uint32_t node = (uint32_t)__ldcg(log + base + r);
+            __pipeline_memcpy_async(stage + 16 * u, vec + (int64_t)node * rb + 16 * c, 16);
+        }
+        __pipeline_commit();
+        __pipeline_wait_prior(0);
+#else
         for (int u = tid; u < nr * upr; u += NT) {
             const int r = u / upr, c = u - r * upr;
             const uint32_t node = (uint32_t)__ldcg(log + base + r);
             reinterpret_cast<uint4 *>(stage)[u] = reinterpret_cast<const uint4 *>(vec + (int64_t)node * rb)[c];
         }
+#endif
         __syncthreads();
         for (int i = tid; i < nr; i += NT) {
             const uint32_t node = (uint32_t)__ldcg(log + base + i);

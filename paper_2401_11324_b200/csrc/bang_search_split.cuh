@@ -46,6 +46,9 @@
 #ifndef BANG_SPLIT_L2HINT
 #define BANG_SPLIT_L2HINT 1
 #endif
+#ifndef BANG_TAB_UNROLL  // table entries (centroid loads) in flight per prologue thread
+#define BANG_TAB_UNROLL 8
+#endif
 
 namespace bang {
 
@@ -764,7 +767,7 @@ __device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qi
     __syncthreads();
     // kernel 1 for this query into shared memory (pq.py:284-296); the
     // centroid loads (L2) of 8 entries per thread are in flight together
-#pragma unroll 8
+#pragma unroll BANG_TAB_UNROLL
     for (int idx = tid; idx < M * 256; idx += NT) {
         const int s = idx >> 8, c = idx & 255;
         float e;
