@@ -49,6 +49,9 @@
 #ifndef BANG_TAB_UNROLL  // table entries (centroid loads) in flight per prologue thread
 #define BANG_TAB_UNROLL 8
 #endif
+namespace bang {
+constexpr int kTabUnroll = BANG_TAB_UNROLL;
+}
 
 namespace bang {
 
@@ -767,7 +770,7 @@ __device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qi
     __syncthreads();
     // kernel 1 for this query into shared memory (pq.py:284-296); the
     // centroid loads (L2) of 8 entries per thread are in flight together
-#pragma unroll BANG_TAB_UNROLL
+#pragma unroll kTabUnroll
     for (int idx = tid; idx < M * 256; idx += NT) {
         const int s = idx >> 8, c = idx & 255;
         float e;
