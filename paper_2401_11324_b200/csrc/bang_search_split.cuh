@@ -46,6 +46,9 @@
 #ifndef BANG_SPLIT_L2HINT
 #define BANG_SPLIT_L2HINT 1
 #endif
+#ifndef BANG_SPLIT_HRPF  // HEADROW also prefetches the staged head's neighbours' code rows
+#define BANG_SPLIT_HRPF 0
+#endif
 #ifndef BANG_TAB_UNROLL  // table entries (centroid loads) in flight per prologue thread
 #define BANG_TAB_UNROLL 8
 #endif
@@ -706,6 +709,14 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
             for (int r = 0; r < PL; ++r)
                 if (lt + 64 * r < p.R) ids[r] = __ldg(hrow + lt + 64 * r);
             if (lt == 0) hv = __ldg(p.deg_share + hid);
+#if BANG_SPLIT_HRPF
+            // and its neighbours' code rows towards L2 (hit if it wins)
+#pragma unroll
+            for (int r = 0; r < PL; ++r)
+                if (lt + 64 * r < p.R && ids[r] >= 0)
+                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.codes + (int64_t)ids[r] * p.code_stride)
+                                 : "memory");
+#endif
         }
         split_bar(5, 128);  // the row warps hold this hop's s_hrow
 #pragma unroll
