@@ -301,8 +301,8 @@ def main():
         return
 
     from paper_2401_11324_b200 import GraphSearcher, _lib, set_device
-    from paper_2401_11324_b200.tools.bench_data import (CONFIGS, EXACT_KNN_LIMIT, HOST_GRAPH_CONFIGS, PARTITIONED,
-                                                        THROUGHPUT_CONFIGS, build_artifacts)
+    from paper_2401_11324_b200.tools.bench_data import (CLUSTER_SCALE, CONFIGS, EXACT_KNN_LIMIT, HOST_GRAPH_CONFIGS,
+                                                        PARTITIONED, THROUGHPUT_CONFIGS, build_artifacts)
     set_device(local)
     thr_only = args.config in THROUGHPUT_CONFIGS
     nq_cfg = 1_000 if args.config == "C1" else (THROUGHPUT_CONFIGS[args.config] if thr_only
@@ -347,6 +347,7 @@ def main():
                         if args.config in PARTITIONED else
                         "GPU IVF kNN(2R) + RobustPrune(1.2) + reverse edges, then search-based Vamana "
                         "passes (t=128, 128, 200) with this search (tools/graph_build.py)"),
+              "cluster_scale": CLUSTER_SCALE.get(args.config, 1.0),
               "l2": "flushed between steps (256 MiB memset outside the step events)",
               "parallelism": f"query-sharded x{ref_world}, index replicated, no collective"}
 

@@ -31,6 +31,13 @@ CONFIGS = {
     "C4": (100_000_000, 10_000, 128, "u8", 1_000_000, 64, 32,
            "SIFT-shape synthetic 100Mx128 uint8, R=64, PQ 32 subspaces, graph + vectors in pinned host memory, "
            "10K queries, k=10"),
+    # C4 with clusters half as wide (cluster_scale 0.5): at 100M points the
+    # default-width mixture has almost no neighbourhood contrast (mean
+    # d10/d100 = 0.78 already at 400K; recall@10 0.54 at t=256 on the real
+    # partitioned graph, profiles/r02/c4/), unlike SIFT; at 0.5 it is 0.42
+    "C4t": (100_000_000, 10_000, 128, "u8", 1_000_000, 64, 32,
+            "SIFT-shape synthetic 100Mx128 uint8 (clusters half as wide), R=64, PQ 32 subspaces, graph + vectors "
+            "in pinned host memory, 10K queries, k=10"),
     # reduced-n variants of the same shapes (parity tests, quick checks)
     "C2s": (100_000, 10_000, 128, "u8", 1_000, 64, 32, "C2 shape at n=100K"),
     "C3s": (200_000, 10_000, 96, "f32", 2_000, 64, 48, "C3 shape at n=200K"),
@@ -41,12 +48,14 @@ CONFIGS = {
 # (graph_build.build_graph_partitioned): parts, overlap, search-based passes
 # per partition.  C4's monolithic build would need ~230 GB of HBM (k-NN
 # candidate tables); C3p checks the partitioned build against C3's.
+CLUSTER_SCALE = {"C4t": 0.5}
 PARTITIONED = {
     "C4": dict(parts=24, overlap=2, refine=(128,)),
+    "C4t": dict(parts=24, overlap=2, refine=(128,)),
     "C3p": dict(parts=4, overlap=2, refine=(128,)),
 }
 # Configs searched with the graph in pinned host memory (BASELINE.json configs[3])
-HOST_GRAPH_CONFIGS = ("C4",)
+HOST_GRAPH_CONFIGS = ("C4", "C4t")
 
 
 # Throughput-only shapes (BASELINE.json configs[3..4]; "C5:
@@ -231,6 +240,7 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
         log(f"[bench_data] {name}: data from checkpoint {ck}")
     else:
         base, queries = gaussian_mixture(n, nq_total, dim, clusters=clusters, seed=seed,
+                                         cluster_scale=CLUSTER_SCALE.get(name, 1.0),
                                          out_dtype=np.uint8 if dt == "u8" else np.float32)
         if dt == "u8":
             queries = queries.astype(np.float32)
@@ -263,9 +273,14 @@ def build_artifacts(name: str, seed: int = 0, nq_total: int | None = None, cache
             graph = GraphIndex(_ck_load(ck, "adjacency"), np.asarray(_ck_load(ck, "degrees")),
                                int(_ck_load(ck, "medoid")), R, validate=False)
         else:
+            # the per-partition checkpoint (an (n, overlap*R) int32 table,
+            # 51 GB at C4) only where the scratch disk holds it
+            import shutil
+            cand_bytes = n * cfg["overlap"] * R * 4
+            part_ck = ck if shutil.disk_usage(ck).free > 1.5 * cand_bytes + 32 * n else None
             graph = build_graph_partitioned(base, degree_bound=R, parts=cfg["parts"], overlap=cfg["overlap"],
                                             refine_fn=refine_fn, refine=cfg["refine"], seed=seed, log=log,
-                                            ckpt_dir=ck)
+                                            ckpt_dir=part_ck)
             _ck_save(ck, adjacency=graph.adjacency, degrees=graph.degrees, medoid=np.int64(graph.medoid))
         t3 = time.time()
         t2, t3 = t3 - (t2 - t1), t3  # report graph time apart from PQ time

@@ -12,14 +12,14 @@ df -h /tmp > $OUT/df_$TAG.txt 2>&1; free -g >> $OUT/df_$TAG.txt; du -sh /tmp/ban
 ( while true; do date +%T; free -g | sed -n 2p; nvidia-smi --query-gpu=memory.used --format=csv,noheader; sleep 60; done ) \
   > $OUT/mem_$TAG.log 2>&1 &
 MON=$!
-timeout ${C4_TIMEOUT:-3300} python bench.py --config C4 --cache "" --steps 5 --warmup 3 \
+timeout ${C4_TIMEOUT:-3300} python bench.py --config ${C4_CONFIG:-C4} --cache "" --steps 5 --warmup 3 \
   > $OUT/bench_C4_$TAG.json 2> $OUT/bench_C4_$TAG.err
 echo "bench C4 rc=$?"
 tail -5 $OUT/bench_C4_$TAG.err
 head -c 1500 $OUT/bench_C4_$TAG.json; echo
 T=$(python -c "import json; print(json.load(open('$OUT/bench_C4_$TAG.json'))['config']['t'])" 2>/dev/null)
 if [ -n "$T" ]; then
-  timeout 900 python bench.py --config C4 --cache "" --kernel split --t $T --no-cpu-baseline --no-parity \
+  timeout 900 python bench.py --config ${C4_CONFIG:-C4} --cache "" --kernel split --t $T --no-cpu-baseline --no-parity \
     > $OUT/bench_C4_split_$TAG.json 2> $OUT/bench_C4_split_$TAG.err
   python -c "import json; d=json.load(open('$OUT/bench_C4_split_$TAG.json')); print('C4 split', d['value'], d['e2e']['value'], d['roofline']['frac'])"
 fi
