@@ -44,7 +44,7 @@
 #define BANG_SPLIT_HEADROW 1
 #endif
 #ifndef BANG_SPLIT_L2HINT
-#define BANG_SPLIT_L2HINT 1
+#define BANG_SPLIT_L2HINT 0
 #endif
 #ifndef BANG_SPLIT_HRPF  // HEADROW also prefetches the staged head's neighbours' code rows
 #define BANG_SPLIT_HRPF 0
@@ -66,47 +66,71 @@ namespace bang {
 // filter's accesses carry an evict_last policy, the code-row gathers
 // evict_first (BANG_SPLIT_L2HINT; the launch's persisting access window
 // sizes the evict_last set).
-#if BANG_SPLIT_L2HINT
+#ifndef BANG_HINT_ATOM
+#define BANG_HINT_ATOM BANG_SPLIT_L2HINT
+#endif
+#ifndef BANG_HINT_LD
+#define BANG_HINT_LD BANG_SPLIT_L2HINT
+#endif
+#ifndef BANG_HINT_ST
+#define BANG_HINT_ST BANG_SPLIT_L2HINT
+#endif
+#ifndef BANG_HINT_CP
+#define BANG_HINT_CP BANG_SPLIT_L2HINT
+#endif
 __device__ __forceinline__ uint64_t l2_keep() {
     uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ uint64_t l2_stream() {
     uint64_t pol;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ uint32_t bloom_or(uint32_t *a, uint32_t v) {
+#if BANG_HINT_ATOM
     uint32_t o;
     asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(l2_keep()) : "memory");
     return o;
+#else
+    return atomicOr(a, v);
+#endif
 }
 __device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) {
+#if BANG_HINT_LD
     uint32_t o;
     asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(l2_keep()) : "memory");
     return o;
+#else
+    return __ldcg(a);
+#endif
 }
 __device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) {
+#if BANG_HINT_ST
     asm volatile("st.global.cg.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_keep()) : "memory");
+#else
+    __stcg(a, v);
+#endif
 }
 __device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) {
+#if BANG_HINT_ST
     asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y),
                  "r"(v.z), "r"(v.w), "l"(l2_keep())
                  : "memory");
+#else
+    __stcg(a, v);
+#endif
 }
 __device__ __forceinline__ void code_copy16(void *dst, const void *src) {
+#if BANG_HINT_CP
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "l"(l2_stream())
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, 16, %2;" ::"r"(sa), "l"(src), "l"(l2_stream())
                  : "memory");
-}
 #else
-__device__ __forceinline__ uint32_t bloom_or(uint32_t *a, uint32_t v) { return atomicOr(a, v); }
-__device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) { return __ldcg(a); }
-__device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) { __stcg(a, v); }
-__device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) { __stcg(a, v); }
-__device__ __forceinline__ void code_copy16(void *dst, const void *src) { __pipeline_memcpy_async(dst, src, 16); }
+    __pipeline_memcpy_async(dst, src, 16);
 #endif
+}
 
 struct SplitMisc {
     unsigned long long rmin[2][2];  // [parity][row warp]: min key of the row's fresh neighbours
