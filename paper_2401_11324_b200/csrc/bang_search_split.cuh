@@ -61,13 +61,14 @@ namespace bang {
 // L2 residency of the per-query Bloom filters.  A query's ~17 K fetch-ors hit
 // random words of its 50 KB filter over ~0.5 ms while ~0.6 GB of code rows,
 // adjacency rows and vectors stream through the 126 MB L2; with default
-// priorities half of the fetch-ors missed L2 (ncu: 109 M of 220 M atomic
-// sectors), putting a DRAM round trip on every hop's critical path.  The
-// filter's accesses carry an evict_last policy, the code-row gathers
-// evict_first (BANG_SPLIT_L2HINT; the launch's persisting access window
-// sizes the evict_last set).
-#ifndef BANG_HINT_ATOM
-#define BANG_HINT_ATOM BANG_SPLIT_L2HINT
+// priorities ncu counted half of the fetch-ors as L2 misses (109 M of 220 M
+// atomic sectors, under ncu's cache control).  The fetch-ors carry an
+// evict_last policy (BANG_HINT_ATOM: +0.5%, so the misses are mostly an
+// artefact of the capture); hinted loads/stores of the filter are neutral,
+// and the hinted cp.async of the code rows faults (illegal instruction) on
+// the B200, so both stay off.
+#ifndef BANG_HINT_ATOM  // measured +0.5% alone (profiles/r02/ab_g/); ld/st hints +0.2%
+#define BANG_HINT_ATOM 1
 #endif
 #ifndef BANG_HINT_LD
 #define BANG_HINT_LD BANG_SPLIT_L2HINT
@@ -75,7 +76,7 @@ namespace bang {
 #ifndef BANG_HINT_ST
 #define BANG_HINT_ST BANG_SPLIT_L2HINT
 #endif
-#ifndef BANG_HINT_CP
+#ifndef BANG_HINT_CP  // the hinted cp.async raised an illegal-instruction fault on the B200
 #define BANG_HINT_CP BANG_SPLIT_L2HINT
 #endif
 __device__ __forceinline__ uint64_t l2_keep() {
