@@ -421,6 +421,10 @@ class GraphSearcher(BaseEstimator):
             parts.append(self.index_.search(q[lo:hi], k, self.t, self.bloom_entries, flags))
             elapsed += time.perf_counter() - t0
         logs = VisitLogs([(p[6], p[7]) for p in parts])
+        if len(parts) == 1:  # one batch: the arrays as returned (no copies)
+            p = parts[0]
+            return SearchResult(ids=p[0], dists=p[1], iterations=p[2], converged=p[3], wall_times=p[5],
+                                elapsed=elapsed, short=p[4], visit_logs=logs)
         return SearchResult(
             ids=np.concatenate([p[0] for p in parts]),
             dists=np.concatenate([p[1] for p in parts]),
