@@ -12,6 +12,7 @@ df -h /tmp > $OUT/df_$TAG.txt 2>&1; free -g >> $OUT/df_$TAG.txt; du -sh /tmp/ban
 ( while true; do date +%T; free -g | sed -n 2p; nvidia-smi --query-gpu=memory.used --format=csv,noheader; sleep 60; done ) \
   > $OUT/mem_$TAG.log 2>&1 &
 MON=$!
+timeout 600 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"; tail -1 $OUT/pytest_gpu_$TAG.log
 timeout ${C4_TIMEOUT:-3300} python bench.py --config ${C4_CONFIG:-C4} --cache "" --steps 5 --warmup 3 \
   > $OUT/bench_C4_$TAG.json 2> $OUT/bench_C4_$TAG.err
 echo "bench C4 rc=$?"
