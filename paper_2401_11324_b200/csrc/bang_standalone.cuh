@@ -49,14 +49,31 @@ __global__ void __launch_bounds__(32 * kShareWarps) row_share_kernel(const int32
             sl[2 * j + 1] = mod_z(fnv1a(id, kFnvOffsetH2), g);
         }
         __syncwarp();
+        // branch-free: every lane holds its (up to) four slots in registers
+        // and compares them with each broadcast slot of the row (R <= 64;
+        // wider rows take the strided loop below)
         bool dup = false;
-        for (int a = lane; a < 2 * d && !dup; a += 32) {
-            const uint32_t v = sl[a];
-            for (int b = 0; b < 2 * d; ++b)
-                if ((b >> 1) != (a >> 1) && sl[b] == v) {
-                    dup = true;
-                    break;
-                }
+        if (d <= 64) {
+            uint32_t v[4];
+            int pa[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int a = lane + 32 * k;
+                v[k] = a < 2 * d ? sl[a] : 0xFFFFFFFFu;  // slots are < z < 2^31: never equal
+                pa[k] = a >> 1;
+            }
+#pragma unroll 8
+            for (int b = 0; b < 2 * d; ++b) {
+                const uint32_t x = sl[b];
+                const int pb = b >> 1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) dup |= (x == v[k]) & (pb != pa[k]);
+            }
+        } else {
+            for (int a = lane; a < 2 * d; a += 32) {
+                const uint32_t v = sl[a];
+                for (int b = 0; b < 2 * d; ++b) dup |= (sl[b] == v) & ((b >> 1) != (a >> 1));
+            }
         }
         const bool shared = __any_sync(kFull, dup);
         if (lane == 0) out[w] = shared ? (int32_t)((uint32_t)d | 0x80000000u) : d;
