@@ -147,6 +147,10 @@ bang_status bang_index_device_ptrs(const bang_index *index, const uint8_t **code
 /* Bytes between device code rows: m, except m = 48 rows padded to 64 bytes
  * (one aligned DRAM burst per gathered row). */
 int32_t bang_index_code_stride(const bang_index *index);
+/* Build the per-(index, bloom_entries) tables of search_split_kernel (each
+ * row's degree with its in-row Bloom slot-sharing flag) now instead of on the
+ * first search at that Bloom size (bang_options.bloom_direct); synchronous. */
+bang_status bang_index_prepare(bang_index *index, int64_t bloom_entries);
 /* Tuning of the searches on this handle (kernel choice and the prefetch
  * kernel's data flows); see bang_options.  Results never depend on it. */
 void bang_options_default(bang_options *options);

@@ -88,6 +88,7 @@ _SIGS = {
     "bang_index_info": (_I32, [_P, _P, _P, _P, _P, _P]),
     "bang_index_device_ptrs": (_I32, [_P, _P, _P, _P, _P, _P]),
     "bang_index_code_stride": (_I32, [_P]),
+    "bang_index_prepare": (_I32, [_P, _I64]),
     "bang_options_default": (None, [ctypes.POINTER(Options)]),
     "bang_index_set_options": (_I32, [_P, ctypes.POINTER(Options)]),
     "bang_index_get_options": (_I32, [_P, ctypes.POINTER(Options)]),

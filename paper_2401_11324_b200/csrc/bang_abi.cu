@@ -1107,6 +1107,17 @@ bang_status bang_index_get_options(const bang_index *ix, bang_options *o) {
 
 int32_t bang_index_code_stride(const bang_index *ix) { return ix ? ix->code_stride : 0; }
 
+bang_status bang_index_prepare(bang_index *ix, int64_t z) {
+    if (!ix) return fail(BANG_E_STATE, "GraphSearcher is not fitted (null index)");
+    if (z < 1 || z >= (1LL << 31)) return fail(BANG_E_PARAM, "bloom_entries must be in [1, 2^31), got %lld", (long long)z);
+    if (!ix->opts.bloom_direct || ix->m <= 0) return BANG_OK;
+    CU(cudaSetDevice(ix->device));
+    bang_status s = ensure_row_share(ix, z, ix->stream);
+    if (s) return s;
+    CU(cudaStreamSynchronize(ix->stream));
+    return BANG_OK;
+}
+
 // ------------------------------------------------------------ per-kernel entries
 
 bang_status bang_pq_table(bang_index *ix, const float *queries, int64_t nq, float *out) {

@@ -343,12 +343,17 @@ class GraphSearcher(BaseEstimator):
         # re-fit (e.g. out of memory) leaves the previous index usable.
         new_index = DeviceIndex(graph, base, codebook, codes, placement, device=getattr(self, "device", None))
         opts = getattr(self, "_kernel_options", None)
-        if opts is not None:
-            try:
+        try:
+            if opts is not None:
                 new_index.set_options(**opts)
-            except Exception:
-                new_index.close()
-                raise
+            if self.mode == "in_memory":
+                # the split kernel's per-(index, Bloom size) row flags now,
+                # not on the first search (bang_index_prepare)
+                _lib.check(_lib.lib().bang_index_prepare(new_index.handle, int(self.bloom_entries)),
+                           "bang_index_prepare")
+        except Exception:
+            new_index.close()
+            raise
         old = getattr(self, "index_", None)
         self.index_ = new_index
         if old is not None:

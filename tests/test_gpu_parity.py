@@ -493,6 +493,22 @@ def test_split_bloom_direct_rows_match_oracle(z, direct):
         _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, 100, zz))
 
 
+def test_index_prepare_then_search():
+    """bang_index_prepare builds the split kernel's row flags ahead of the
+    search (fit does it for the searcher's Bloom size); results unchanged."""
+    base, q, graph, cb, codes = _random_case(31, 20_000, 96, 64, 48, 100, np.float32)
+    s = B.GraphSearcher(k=10, t=64, mode="in_memory", bloom_entries=20_011, debug_checks=True)
+    s.fit(base, graph=graph, codebook=cb, codes=codes)
+    L = B._lib.lib()
+    B._lib.check(L.bang_index_prepare(s.index_.handle, 4099))
+    with pytest.raises(B.ParameterError):
+        B._lib.check(L.bang_index_prepare(s.index_.handle, 0))
+    for z in (20_011, 4099):
+        s.bloom_entries = z
+        res = s.set_kernel("split").search(q)
+        _same_as_oracle(res, _oracle_search(q, graph, cb, codes, base, 64, z))
+
+
 @pytest.mark.parametrize("seed,n,d,R,m,t,dtype", [
     (23, 16_000, 96, 100, 48, 120, np.float32),  # 64 < R <= 128: two slots per row thread
     (24, 16_000, 128, 128, 32, 200, np.uint8),
