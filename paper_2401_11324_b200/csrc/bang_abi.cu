@@ -147,7 +147,6 @@ struct bang_index {
     DevBuf<int32_t> retry_log;
     // degree | in-row Bloom slot sharing << 31 at z = row_share_z (bloom_direct)
     DevBuf<int32_t> row_share;
-    DevBuf<uint32_t> share_bits;  // the same flags, one bit per node
     int64_t row_share_z = 0;
 };
 
@@ -461,7 +460,6 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.off_hrow = pl.off_hrow;
     p.row_prefetch = o.row_prefetch != 0;
     p.deg_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
-    p.share_bits = p.deg_share ? ix->share_bits.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
     CU(cudaMemsetAsync(ix->counters.p, 0, sizeof(unsigned long long) * kCtrT0, st));
     CU(cudaMemsetAsync(ix->counters.p + kCtrPhase0, 0, sizeof(unsigned long long) * 8, st));
@@ -532,14 +530,12 @@ bang_status ensure_row_share(bang_index *ix, int64_t z, cudaStream_t st) {
     if (ix->row_share_z == z) return BANG_OK;
     bang_status s = ix->row_share.reserve((size_t)ix->n);
     if (s) return s;
-    if ((s = ix->share_bits.reserve((size_t)ceil_div(ix->n, 32)))) return s;
-    CU(cudaMemsetAsync(ix->share_bits.p, 0, sizeof(uint32_t) * ceil_div(ix->n, 32), st));
     BloomGeom g;
     g.z = (uint64_t)z;
     g.magic = ~0ull / (uint64_t)z;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(ix->n, kShareWarps), (int64_t)ix->sm_count * 16));
     row_share_kernel<<<(unsigned)blocks, 32 * kShareWarps, sizeof(uint32_t) * kShareWarps * 2 * ix->R, st>>>(
-        ix->adj, ix->adj_stride, ix->deg, ix->n, ix->R, g, ix->row_share.p, ix->share_bits.p);
+        ix->adj, ix->adj_stride, ix->deg, ix->n, ix->R, g, ix->row_share.p);
     CU(cudaGetLastError());
     ix->row_share_z = z;
     return BANG_OK;
@@ -841,7 +837,6 @@ void bang_index_destroy(bang_index *ix) {
     ix->skip.release();
     ix->retry_log.release();
     ix->row_share.release();
-    ix->share_bits.release();
     for (auto e : ix->ev)
         if (e) cudaEventDestroy(e);
     if (ix->stream) cudaStreamDestroy(ix->stream);

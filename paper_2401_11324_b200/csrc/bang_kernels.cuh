@@ -98,7 +98,6 @@ struct SearchParams {
     // at this z; rows without it take their pre-state bits from the
     // fetch-or.  Read in place of deg (one load).  nullptr: off
     const int32_t *deg_share;
-    const uint32_t *share_bits;  // the same flags as a bitset (A/B builds)
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {

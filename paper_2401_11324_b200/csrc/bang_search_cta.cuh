@@ -19,11 +19,6 @@
 
 #include "bang_kernels.cuh"
 
-// A/B switch (scripts/build_variant.sh): re-rank rows staged by cp.async
-#ifndef BANG_RERANK_ASYNC
-#define BANG_RERANK_ASYNC 1
-#endif
-
 namespace bang {
 
 struct CtaMisc {
@@ -59,7 +54,6 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
         // the rows' 16-byte pieces by cp.async (no register round trip); the
         // log reads of 8 pieces are in flight together, so a chunk costs a few
         // L2 round trips and one HBM round trip, not one of each per piece
-#if BANG_RERANK_ASYNC
 #pragma unroll 8
         for (int u = tid; u < nr * upr; u += NT) {
             const int r = u / upr, c = u - r * upr;
@@ -68,13 +62,6 @@ __device__ __forceinline__ void rerank_staged(const SearchParams &p, const int32
         }
         __pipeline_commit();
         __pipeline_wait_prior(0);
-#else
-        for (int u = tid; u < nr * upr; u += NT) {
-            const int r = u / upr, c = u - r * upr;
-            const uint32_t node = (uint32_t)__ldcg(log + base + r);
-            reinterpret_cast<uint4 *>(stage)[u] = reinterpret_cast<const uint4 *>(vec + (int64_t)node * rb)[c];
-        }
-#endif
         __syncthreads();
         for (int i = tid; i < nr; i += NT) {
             const uint32_t node = (uint32_t)__ldcg(log + base + i);

@@ -27,111 +27,39 @@
 
 #include "bang_search_cta.cuh"
 
-// A/B switches of the experiment builds (scripts/build_variant.sh)
-#ifndef BANG_SPLIT_BITSET
-#define BANG_SPLIT_BITSET 0
-#endif
-#ifndef BANG_SPLIT_O2COPY
-#define BANG_SPLIT_O2COPY 1
-#endif
-#ifndef BANG_SPLIT_LIST2
-#define BANG_SPLIT_LIST2 1
-#endif
-#ifndef BANG_SPLIT_HEADPF
-#define BANG_SPLIT_HEADPF 0
-#endif
-#ifndef BANG_SPLIT_HEADROW
-#define BANG_SPLIT_HEADROW 1
-#endif
-#ifndef BANG_SPLIT_L2HINT
-#define BANG_SPLIT_L2HINT 0
-#endif
-#ifndef BANG_SPLIT_HRPF  // HEADROW also prefetches the staged head's neighbours' code rows
-#define BANG_SPLIT_HRPF 0
-#endif
-#ifndef BANG_TAB_UNROLL  // table entries (centroid loads) in flight per prologue thread
+// table entries (centroid loads) in flight per prologue thread (8, 16 and
+// 24 measured equal, profiles/r02/ab_h/)
+#ifndef BANG_TAB_UNROLL
 #define BANG_TAB_UNROLL 8
 #endif
-namespace bang {
-constexpr int kTabUnroll = BANG_TAB_UNROLL;
-}
 
 namespace bang {
+
+constexpr int kTabUnroll = BANG_TAB_UNROLL;
 
 // L2 residency of the per-query Bloom filters.  A query's ~17 K fetch-ors hit
 // random words of its 50 KB filter over ~0.5 ms while ~0.6 GB of code rows,
-// adjacency rows and vectors stream through the 126 MB L2; with default
-// priorities ncu counted half of the fetch-ors as L2 misses (109 M of 220 M
-// atomic sectors, under ncu's cache control).  The fetch-ors carry an
-// evict_last policy (BANG_HINT_ATOM: +0.5%, so the misses are mostly an
-// artefact of the capture); hinted loads/stores of the filter are neutral,
-// and the hinted cp.async of the code rows faults (illegal instruction) on
-// the B200, so both stay off.
-#ifndef BANG_HINT_ATOM  // measured +0.5% alone (profiles/r02/ab_g/); ld/st hints +0.2%
-#define BANG_HINT_ATOM 1
-#endif
-#ifndef BANG_HINT_LD
-#define BANG_HINT_LD BANG_SPLIT_L2HINT
-#endif
-#ifndef BANG_HINT_ST
-#define BANG_HINT_ST BANG_SPLIT_L2HINT
-#endif
-#ifndef BANG_HINT_CP  // the hinted cp.async raised an illegal-instruction fault on the B200
-#define BANG_HINT_CP BANG_SPLIT_L2HINT
-#endif
+// adjacency rows and vectors stream through the 126 MB L2; ncu counted half
+// of the fetch-ors as L2 misses (109 M of 220 M atomic sectors, under ncu's
+// cache control).  The fetch-ors carry an evict_last policy (+0.5%, so the
+// misses are mostly an artefact of the capture); hinted loads/stores of the
+// filter measured neutral and a hinted cp.async of the code rows faulted
+// (illegal instruction) on the B200, so those stay plain
+// (profiles/r02/ab_g/, ab_h/).
 __device__ __forceinline__ uint64_t l2_keep() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-__device__ __forceinline__ uint64_t l2_stream() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
 __device__ __forceinline__ uint32_t bloom_or(uint32_t *a, uint32_t v) {
-#if BANG_HINT_ATOM
     uint32_t o;
     asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;" : "=r"(o) : "l"(a), "r"(v), "l"(l2_keep()) : "memory");
     return o;
-#else
-    return atomicOr(a, v);
-#endif
 }
-__device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) {
-#if BANG_HINT_LD
-    uint32_t o;
-    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(o) : "l"(a), "l"(l2_keep()) : "memory");
-    return o;
-#else
-    return __ldcg(a);
-#endif
-}
-__device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) {
-#if BANG_HINT_ST
-    asm volatile("st.global.cg.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(a), "r"(v), "l"(l2_keep()) : "memory");
-#else
-    __stcg(a, v);
-#endif
-}
-__device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) {
-#if BANG_HINT_ST
-    asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w), "l"(l2_keep())
-                 : "memory");
-#else
-    __stcg(a, v);
-#endif
-}
-__device__ __forceinline__ void code_copy16(void *dst, const void *src) {
-#if BANG_HINT_CP
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, 16, %2;" ::"r"(sa), "l"(src), "l"(l2_stream())
-                 : "memory");
-#else
-    __pipeline_memcpy_async(dst, src, 16);
-#endif
-}
+__device__ __forceinline__ uint32_t bloom_ld(const uint32_t *a) { return __ldcg(a); }
+__device__ __forceinline__ void bloom_st(uint32_t *a, uint32_t v) { __stcg(a, v); }
+__device__ __forceinline__ void bloom_st4(uint4 *a, uint4 v) { __stcg(a, v); }
+__device__ __forceinline__ void code_copy16(void *dst, const void *src) { __pipeline_memcpy_async(dst, src, 16); }
 
 struct SplitMisc {
     unsigned long long rmin[2][2];  // [parity][row warp]: min key of the row's fresh neighbours
@@ -146,7 +74,6 @@ struct SplitMisc {
     int opos;                    // list warps: old position of okey (cnt if none)
     int coll;                    // row warps: in-row slot sharing seen
     long long qi;
-    unsigned long long pfh;      // list warps: head whose neighbours' code rows went to L2 (HEADPF)
     uint32_t hid;                // HEADROW: node whose row ids are staged in s_hrow (~0u: none)
     int32_t hdeg;                // HEADROW: its deg_share word
     unsigned long long ph[8];  // phase profiler
@@ -295,7 +222,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     int deg;
     bool shared = true;  // in-row slot sharing at this z (unknown: the exact path)
     bool pre = false;
-#if BANG_SPLIT_HEADROW
     // The list warps staged the published head's row ids + deg_share word
     // (68% of hops expand the old head): no adjacency read then.  Every hop
     // h >= 1 the row warps arrive on barrier 5 once they hold s_hrow, so the
@@ -317,18 +243,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     }
     if (pre) {
     } else
-#endif
-#if BANG_SPLIT_BITSET
-    // (A/B variant: the flag from a bitset beside the degree array)
-    if (p.deg_share) {
-        const uint32_t sw = __ldg(p.share_bits + (w >> 5));
-        deg = p.host_graph ? (p.row_hdr ? row[-4] : p.deg[w]) : __ldg(p.deg + w);
-        shared = (sw >> (w & 31)) & 1u;
-#pragma unroll
-        for (int r = 0; r < PL; ++r)
-            nid[r] = rt + 64 * r < p.R ? (uint32_t)(p.host_graph ? row[rt + 64 * r] : __ldg(row + rt + 64 * r)) : 0u;
-    } else
-#endif
     if (p.deg_share) {
         // degree + sharing flag in one load (HBM; host-mapped rows too)
         const int32_t v = __ldg(p.deg_share + w);
@@ -385,11 +299,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             // profiles/r02/ab_v4/)
             if (on[r]) {
                 o1[r] = bloom_or(bits + (p1[r] >> 5), 1u << (p1[r] & 31));
-#if BANG_SPLIT_O2COPY
                 o2[r] = p2[r] != p1[r] ? bloom_or(bits + (p2[r] >> 5), 1u << (p2[r] & 31)) : o1[r];
-#else
-                if (p2[r] != p1[r]) o2[r] = bloom_or(bits + (p2[r] >> 5), 1u << (p2[r] & 31));
-#endif
             }
         }
         SPLIT_STAMP(1, p1[0])
@@ -563,7 +473,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     const int c0w = s_m->wsurv[0], c1w = s_m->wsurv[1];
     const int n = c0w + c1w;
     SPLIT_STAMP(0, n)
-#if BANG_SPLIT_LIST2
     // ---- kernels 4a + 4b in one pass over the (unsorted) survivors, from
     // the same broadcast reads: each survivor's rank among them (its sorted
     // slot) and each old entry's count of smaller survivors (keys are unique)
@@ -603,48 +512,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     }
     SPLIT_STAMP(1, 0)
     SPLIT_STAMP(2, mc[0])
-#else
-    // ---- kernel 4a: rank sort of the survivors (broadcast reads)
-#pragma unroll
-    for (int r = 0; r < PL; ++r) {
-        if (sv[r]) {
-            int rk = 0;
-            for (int i = 0; i < c0w; ++i) rk += s_nk[i] < k[r];
-            for (int i = 0; i < c1w; ++i) rk += s_nk[H + i] < k[r];
-            s_sk[rk] = k[r];
-        }
-    }
-    split_bar(4, NC);
-    SPLIT_STAMP(1, 0)
-    // ---- kernel 4b: each old entry's count of smaller survivors (the
-    // chunks' binary searches interleaved step by step)
-    const int nch = (cnt + NC - 1) / NC;
-    uint64_t mv[MAXCH];
-    uint8_t mvv[MAXCH];
-    int mc[MAXCH];
-#pragma unroll
-    for (int c = 0; c < MAXCH; ++c) {
-        const int i = c * NC + lt;
-        mv[c] = kSentinel;
-        mvv[c] = 0;
-        mc[c] = 0;
-        if (c < nch && i < cnt) {
-            mv[c] = s_wl[i];
-            mvv[c] = s_vis[i];
-        }
-    }
-    if (n > 0) {
-        for (int step = 1 << (31 - __clz(n)); step > 0; step >>= 1) {
-#pragma unroll
-            for (int c = 0; c < MAXCH; ++c)
-                if (c < nch && mc[c] + step <= n && s_sk[mc[c] + step - 1] < mv[c]) mc[c] += step;
-        }
-#pragma unroll
-        for (int c = 0; c < MAXCH; ++c)
-            if (c < nch && c * NC + lt < cnt) s_c[c * NC + lt] = (int16_t)mc[c];
-    }
-    SPLIT_STAMP(2, mc[0])
-#endif
     split_bar(4, NC);  // all reads of the old worklist precede the writes
     // ---- merge + truncate to t (engine.py:210-215): old entry i goes to
     // i + c_i; survivors c_{i-1} .. c_i - 1 land just before it, the rest
@@ -715,7 +582,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
         // the head may be the next winner: its row to L2
         if (p.row_prefetch && hk != kSentinel) prefetch_row_l2(p, key_id(hk));
     }
-#if BANG_SPLIT_HEADROW
     // stage the published head's row ids + deg_share word for the row warps
     // (used when it wins the next hop); the loads run in the list warps'
     // slack before the hop barrier
@@ -734,14 +600,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
             for (int r = 0; r < PL; ++r)
                 if (lt + 64 * r < p.R) ids[r] = __ldg(hrow + lt + 64 * r);
             if (lt == 0) hv = __ldg(p.deg_share + hid);
-#if BANG_SPLIT_HRPF
-            // and its neighbours' code rows towards L2 (hit if it wins)
-#pragma unroll
-            for (int r = 0; r < PL; ++r)
-                if (lt + 64 * r < p.R && ids[r] >= 0)
-                    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p.codes + (int64_t)ids[r] * p.code_stride)
-                                 : "memory");
-#endif
         }
         split_bar(5, 128);  // the row warps hold this hop's s_hrow
 #pragma unroll
@@ -751,25 +609,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
             s_m->hid = hid;
         }
     }
-#endif
-#if BANG_SPLIT_HEADPF
-    // A head that stays the head (its adjacency row went to L2 a hop ago,
-    // so this read hits) gets its neighbours' code rows prefetched to L2:
-    // if it wins the next hop, the row warps' gathers hit L2.  Once per head.
-    if (!p.host_graph) {
-        split_bar(4, NC);  // the published head
-        const uint64_t hk2 = s_m->head[nxt];
-        if (hk2 != kSentinel && hk2 == head && s_m->pfh != hk2) {
-            const int32_t *hrow = p.adj + (int64_t)key_id(hk2) * p.adj_stride;
-            for (int j = lt; j < p.R; j += NC) {
-                const int32_t id = __ldg(hrow + j);
-                if (id >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.codes + (int64_t)id * p.code_stride) : "memory");
-            }
-            split_bar(4, NC);  // every list thread has read pfh
-            if (lt == 0) s_m->pfh = hk2;
-        }
-    }
-#endif
     SPLIT_STAMP(4, 0)
     if (bk) {  // hop statistics: expansions of the old head, survivors merged
         s_m->ph[5] += won_head;
@@ -967,7 +806,6 @@ __global__ void __launch_bounds__(128, MV == 3 ? 4 : 5) search_split_kernel(cons
             s_m->hpos[0] = 1;
             s_m->thr[0] = t == 1 ? s_wl[0] : kSentinel;
             s_m->cnt[0] = 1;
-            s_m->pfh = kSentinel;
             s_m->hid = 0xFFFFFFFFu;
         }
         if (p.profile && tid == 0) {

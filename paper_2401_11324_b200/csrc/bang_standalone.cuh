@@ -34,8 +34,7 @@ __global__ void __launch_bounds__(32 * kShareWarps) row_share_kernel(const int32
                                                                      int64_t adj_stride,
                                                                      const int32_t *__restrict__ deg,
                                                                      int64_t n, int R, BloomGeom g,
-                                                                     int32_t *__restrict__ out,
-                                                                     uint32_t *__restrict__ bits) {
+                                                                     int32_t *__restrict__ out) {
     extern __shared__ uint32_t s_slots[];  // [kShareWarps][2R]
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     uint32_t *sl = s_slots + wi * 2 * R;
@@ -77,7 +76,6 @@ __global__ void __launch_bounds__(32 * kShareWarps) row_share_kernel(const int32
         }
         const bool shared = __any_sync(kFull, dup);
         if (lane == 0) out[w] = shared ? (int32_t)((uint32_t)d | 0x80000000u) : d;
-        if (lane == 0 && shared) atomicOr(bits + (w >> 5), 1u << (w & 31));
         __syncwarp();
     }
 }
