@@ -50,7 +50,7 @@ class Options(ctypes.Structure):
     _fields_ = [
         ("kernel", ctypes.c_int32), ("row_prefetch", ctypes.c_int32), ("bloom_clear", ctypes.c_int32),
         ("l2_persist", ctypes.c_int32), ("profile", ctypes.c_int32), ("bloom_direct", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 10),
+        ("head_row", ctypes.c_int32), ("reserved", ctypes.c_int32 * 9),
     ]
 
     def as_dict(self):

@@ -458,6 +458,7 @@ bang_status launch_pass(bang_index *ix, const Plan &pl, const float *d_queries, 
     p.bloom_clear = o.bloom_clear != 0;
     p.off_code = pl.off_code;
     p.off_hrow = pl.off_hrow;
+    p.head_row = o.head_row != 0;
     p.row_prefetch = o.row_prefetch != 0;
     p.deg_share = pl.kernel == kKSplit && o.bloom_direct && ix->row_share_z == z ? ix->row_share.p : nullptr;
     // reset the per-pass counters (next-query, stats, overflow) but keep t0
@@ -1084,6 +1085,7 @@ void bang_options_default(bang_options *o) {
     o->l2_persist = 1;
     o->profile = 0;
     o->bloom_direct = 1;
+    o->head_row = 1;
 }
 
 bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {

@@ -89,7 +89,8 @@ struct SearchParams {
     // search_split_kernel: the row keys (double-buffered) at off_code
     int32_t off_code;
     // search_split_kernel: the head's row ids staged by the list warps
-    int32_t off_hrow;
+    // (bang_options.head_row)
+    int32_t off_hrow, head_row;
     // code row stride in bytes (m, or m rounded up to 64 B for m = 48:
     // one DRAM burst per gathered row)
     int32_t code_stride;

@@ -226,7 +226,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     // (68% of hops expand the old head): no adjacency read then.  Every hop
     // h >= 1 the row warps arrive on barrier 5 once they hold s_hrow, so the
     // list warps may overwrite it (they sync on 5 late in the hop).
-    if (hop1 && p.deg_share && !p.host_graph) {
+    if (hop1 && p.head_row && p.deg_share && !p.host_graph) {
         uint32_t dep = 0;
         if (s_m->hid == w) {
             pre = true;
@@ -585,7 +585,7 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     // stage the published head's row ids + deg_share word for the row warps
     // (used when it wins the next hop); the loads run in the list warps'
     // slack before the hop barrier
-    if (p.deg_share && !p.host_graph) {
+    if (p.head_row && p.deg_share && !p.host_graph) {
         split_bar(4, NC);  // the published head
         const uint64_t hk2 = s_m->head[nxt];
         int32_t ids[PL];

@@ -471,8 +471,8 @@ def test_split_kernel_large_t_matches_oracle(shape, t):
 
 
 @pytest.mark.parametrize("z", [20_011, 399_887])
-@pytest.mark.parametrize("direct", [0, 1])
-def test_split_bloom_direct_rows_match_oracle(z, direct):
+@pytest.mark.parametrize("direct,head_row", [(0, 1), (1, 1), (1, 0)])
+def test_split_bloom_direct_rows_match_oracle(z, direct, head_row):
     """bloom_direct: rows without in-row slot sharing (a per-(index, z)
     bitset) take their pre-state bits from the fetch-or, the others the
     pre-state read + replay.  z = 20,011 flags about a third of the rows, so
@@ -485,7 +485,7 @@ def test_split_bloom_direct_rows_match_oracle(z, direct):
     graph = B.GraphIndex(adj, graph.degrees, graph.medoid, graph.degree_bound, validate=False)
     s = B.GraphSearcher(k=10, t=100, mode="in_memory", bloom_entries=z, debug_checks=True)
     s.fit(base, graph=graph, codebook=cb, codes=codes)
-    s.set_kernel("split", bloom_direct=direct)
+    s.set_kernel("split", bloom_direct=direct, head_row=head_row)
     for zz in (z, 4099, z):
         s.bloom_entries = zz
         res = s.search(q)
