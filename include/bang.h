@@ -79,9 +79,8 @@ typedef struct bang_options {
     int32_t bloom_direct; /* 1 (split): rows without in-row Bloom slot sharing (a per-(index,
                              z) bitset, built once) read their pre-state from the fetch-or
                              itself -- no separate pre-state read and no row barrier     */
-    int32_t head_row;     /* split kernel, HBM graph, with bloom_direct: the list warps stage the
-                             published head's adjacency row in shared memory for the next hop
-                             (1), and its Bloom slots (2, default); 0: off                 */
+    int32_t head_row;     /* 1 (split, HBM graph, with bloom_direct): the list warps stage the
+                             published head's adjacency row in shared memory for the next hop */
     int32_t reserved[9];
 } bang_options;
 

@@ -218,10 +218,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         pl.kernel = kKSplit;
         int off = 0;
         auto take = [&](int64_t bytes) { const int o_ = off; off += (int)align_up(bytes, 16); return o_; };
-        // the query (prologue + epilogue only) shares its slot with the
-        // head row staged during the hops: ids + two Bloom slots per entry
-        pl.off_q = take(std::max<int64_t>(4LL * ix->dim, 12LL * srpad));
-        pl.off_hrow = pl.off_q;
+        pl.off_q = take(4LL * ix->dim);
         pl.off_wl = take(8LL * t);
         pl.off_sk = take(8LL * srpad);
         pl.off_nk = take(8LL * srpad);
@@ -230,6 +227,7 @@ bang_status make_plan(bang_index *ix, int64_t nq, int t, int64_t z, int flags, P
         // staged code rows (16*MV bytes each); the replay records reuse it
         pl.off_dup = take(std::max<int64_t>(16LL * mv * srpad, 10LL * srpad));
         pl.off_alive = take(srpad);        // replay output
+        pl.off_hrow = take(4LL * srpad);   // the head's row ids, staged by the list warps
         pl.off_acc = take(256);            // SplitMisc
         pl.off_vis = take(t);
         pl.off_tab = take(tab_bytes);
@@ -1087,7 +1085,7 @@ void bang_options_default(bang_options *o) {
     o->l2_persist = 1;
     o->profile = 0;
     o->bloom_direct = 1;
-    o->head_row = 2;
+    o->head_row = 1;
 }
 
 bang_status bang_index_set_options(bang_index *ix, const bang_options *o) {

@@ -221,8 +221,7 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     uint32_t nid[PL];
     int deg;
     bool shared = true;  // in-row slot sharing at this z (unknown: the exact path)
-    bool pre = false, pre_h = false;
-    uint32_t hp1[PL], hp2[PL];
+    bool pre = false;
     // The list warps staged the published head's row ids + deg_share word
     // (68% of hops expand the old head): no adjacency read then.  Every hop
     // h >= 1 the row warps arrive on barrier 5 once they hold s_hrow, so the
@@ -238,15 +237,6 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             for (int r = 0; r < PL; ++r) {
                 nid[r] = rt + 64 * r < p.R ? (uint32_t)s_hrow[rt + 64 * r] : 0u;
                 dep ^= nid[r];
-            }
-            if (p.head_row == 2) {  // and their Bloom slots (head_row 2)
-                pre_h = true;
-#pragma unroll
-                for (int r = 0; r < PL; ++r) {
-                    hp1[r] = (uint32_t)s_hrow[64 * PL + rt + 64 * r];
-                    hp2[r] = (uint32_t)s_hrow[128 * PL + rt + 64 * r];
-                    dep ^= hp1[r] ^ hp2[r];
-                }
             }
         }
         asm volatile("bar.arrive 5, 128;" ::"r"(dep) : "memory");
@@ -290,8 +280,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
             on[r] = rt + 64 * r < deg;
             p1[r] = p2[r] = 0u;
             if (on[r]) {
-                p1[r] = pre_h ? hp1[r] : mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
-                p2[r] = pre_h ? hp2[r] : mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
+                p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
+                p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
                 const uint8_t *crow = p.codes + (int64_t)nid[r] * p.code_stride;
 #pragma unroll
                 for (int v = 0; v < MV; ++v)
@@ -332,8 +322,8 @@ __device__ __forceinline__ void split_row(const SearchParams &p, uint32_t w, int
     for (int r = 0; r < PL; ++r) {
         p1[r] = p2[r] = wd1[r] = wd2[r] = 0u;
         if (rt + 64 * r < deg) {
-            p1[r] = pre_h ? hp1[r] : mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
-            p2[r] = pre_h ? hp2[r] : mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
+            p1[r] = mod_z(fnv1a(nid[r], kFnvOffset), p.geom);
+            p2[r] = mod_z(fnv1a(nid[r], kFnvOffsetH2), p.geom);
             wd1[r] = bloom_ld(bits + (p1[r] >> 5));
             wd2[r] = bloom_ld(bits + (p2[r] >> 5));
         }
@@ -611,24 +601,9 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
                 if (lt + 64 * r < p.R) ids[r] = __ldg(hrow + lt + 64 * r);
             if (lt == 0) hv = __ldg(p.deg_share + hid);
         }
-        uint32_t h1[PL], h2[PL];
-        if (p.head_row == 2) {  // the row's Bloom slots too (bloom.py:26-42)
-#pragma unroll
-            for (int r = 0; r < PL; ++r) {
-                h1[r] = mod_z(fnv1a((uint32_t)ids[r], kFnvOffset), p.geom);
-                h2[r] = mod_z(fnv1a((uint32_t)ids[r], kFnvOffsetH2), p.geom);
-            }
-        }
         split_bar(5, 128);  // the row warps hold this hop's s_hrow
 #pragma unroll
         for (int r = 0; r < PL; ++r) s_hrow[lt + 64 * r] = ids[r];
-        if (p.head_row == 2) {
-#pragma unroll
-            for (int r = 0; r < PL; ++r) {
-                s_hrow[64 * PL + lt + 64 * r] = (int32_t)h1[r];
-                s_hrow[128 * PL + lt + 64 * r] = (int32_t)h2[r];
-            }
-        }
         if (lt == 0) {
             s_m->hdeg = hv;
             s_m->hid = hid;
@@ -713,7 +688,7 @@ __device__ __forceinline__ void split_prologue(const SearchParams &p, int64_t qi
 // overflowed (the host re-runs the query).
 template <int MV>
 __device__ __forceinline__ int split_epilogue(const SearchParams &p, int64_t qid, int iters, int cnt,
-                                           const int32_t *log, float *s_q, const uint64_t *s_wl,
+                                           const int32_t *log, const float *s_q, const uint64_t *s_wl,
                                            float *s_tab, uint64_t *rr) {
     constexpr int M = 16 * MV;
     const int tid = threadIdx.x;
@@ -747,9 +722,7 @@ __device__ __forceinline__ int split_epilogue(const SearchParams &p, int64_t qid
         }
         return 0;
     }
-    // kernel 5: exact distances of the visit log, then top-k (warp 0).  The
-    // query's smem slot held the staged head rows during the hops: reload it.
-    for (int i = tid; i < p.dim; i += 128) s_q[i] = __ldg(p.queries + qid * p.dim + i);
+    // kernel 5: exact distances of the visit log, then top-k (warp 0)
     __threadfence_block();
     __syncthreads();
     const int rowb = p.dim * (p.vec_dtype == kVecF32 ? 4 : 1);
