@@ -513,27 +513,6 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     SPLIT_STAMP(1, 0)
     SPLIT_STAMP(2, mc[0])
     split_bar(4, NC);  // all reads of the old worklist precede the writes
-    // head_row 2: the next head is min(next old unvisited entry, best survivor
-    // other than the winner) unless truncated -- known now, so its row loads
-    // run under the scatter and the expansion below
-    const bool hr_early = p.head_row == 2 && p.deg_share && !p.host_graph;
-    uint64_t hcand = kSentinel;
-    int32_t eids[PL];
-    int32_t ehv = 0;
-    if (hr_early) {
-        const uint64_t skr0 = (won_head ? 0 : 1) < n ? s_sk[won_head ? 0 : 1] : kSentinel;
-        const uint64_t ok0 = s_m->okey;
-        hcand = skr0 < ok0 ? skr0 : ok0;
-#pragma unroll
-        for (int r = 0; r < PL; ++r) eids[r] = 0;
-        if (hcand != kSentinel) {
-            const int32_t *hrow = p.adj + (int64_t)key_id(hcand) * p.adj_stride;
-#pragma unroll
-            for (int r = 0; r < PL; ++r)
-                if (lt + 64 * r < p.R) eids[r] = __ldg(hrow + lt + 64 * r);
-            if (lt == 0) ehv = __ldg(p.deg_share + key_id(hcand));
-        }
-    }
     // ---- merge + truncate to t (engine.py:210-215): old entry i goes to
     // i + c_i; survivors c_{i-1} .. c_i - 1 land just before it, the rest
     // after the last old entry
@@ -606,19 +585,7 @@ __device__ __forceinline__ void split_list(const SearchParams &p, int lt, uint64
     // stage the published head's row ids + deg_share word for the row warps
     // (used when it wins the next hop); the loads run in the list warps'
     // slack before the hop barrier
-    if (hr_early) {
-        // the loads issued after the merge counts; staged only if the
-        // published head is that candidate (else it was truncated)
-        split_bar(4, NC);  // the published head
-        const uint64_t hk2 = s_m->head[nxt];
-        split_bar(5, 128);  // the row warps hold this hop's s_hrow
-#pragma unroll
-        for (int r = 0; r < PL; ++r) s_hrow[lt + 64 * r] = eids[r];
-        if (lt == 0) {
-            s_m->hdeg = ehv;
-            s_m->hid = hk2 == hcand && hk2 != kSentinel ? key_id(hk2) : 0xFFFFFFFFu;
-        }
-    } else if (p.head_row && p.deg_share && !p.host_graph) {
+    if (p.head_row && p.deg_share && !p.host_graph) {
         split_bar(4, NC);  // the published head
         const uint64_t hk2 = s_m->head[nxt];
         int32_t ids[PL];
